@@ -1,0 +1,163 @@
+/* mcsg — B200-native McSplit (maximum common induced subgraph) solver.
+ *
+ * C ABI of the drop-in boundary. Plain pointers and sizes, caller-owned
+ * buffers, no allocation across the ABI, integer status codes. Each entry
+ * point replaces one public entry of the reference C++ solver
+ * (/root/reference/proj/include/mcs/...):
+ *
+ *   mcsg_solve                 mcs::solve(g, h, SolveConfig)              solve.hpp:128
+ *                              (mode MCSG_MODE_PARITY reproduces it node-for-node;
+ *                               MCSG_MODE_THROUGHPUT is the GPU work-sharing engine)
+ *   mcsg_solve_parallel        mcs::solve_parallel(g, h, ParallelConfig)  engine_parallel.hpp:16
+ *   mcsg_solve_batch           run_suite's per-instance loop              bench.cpp:74-122
+ *                              (many pairs in one persistent launch)
+ *   mcsg_solve_goal_directed   mcs::solve_goal_directed                   solve.hpp:132
+ *   mcsg_bound_jump            mcs::bound_jump_search                     heuristics.hpp:69
+ *   mcsg_portfolio             mcs::run_portfolio (race semantics)        portfolio.hpp:100
+ *   mcsg_verify                mcs::oracle::verify                        oracle.hpp:16
+ *   mcsg_random_graph          mcs::random_graph                          graph.hpp:99
+ *   mcsg_random_permutation    mcs::random_permutation                    graph.hpp:102
+ *   mcsg_ordering              mcs::make_ordering                         heuristics.hpp:26
+ *   mcsg_load_graph_file       mcs::load_graph_file                       graph_io.hpp:33
+ *   mcsg_save_graph_file       mcs::save_graph_file                       graph_io.hpp:34
+ *   mcsg_pack_graph            (the loader's bitset packing; no reference counterpart)
+ *
+ * Graphs use the reference's storage: an n*n row-major byte matrix of
+ * adjacency codes (graph.hpp:40,60): 0 none; undirected 1 = edge; directed
+ * 1 forward (u->v), 2 backward, 3 both, mirror-consistent.
+ *
+ * Errors: functions return MCSG_ERROR (and mcsg_last_error() explains) where
+ * the reference throws GraphError / ParseError; timeouts and cancellation are
+ * statuses, not errors (solve.hpp:23). No CPU fallback: without a usable CUDA
+ * device every solve returns MCSG_ERROR.
+ */
+#ifndef MCSG_H
+#define MCSG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCSG_ABI_VERSION 1
+
+/* status codes (mirror mcs_main.cpp:22-24 exit codes; SolveStatus solve.hpp:23) */
+#define MCSG_OPTIMAL 0
+#define MCSG_TIMEOUT 2
+#define MCSG_ERROR 3
+#define MCSG_CANCELLED 4
+
+/* mcsg_graph.flags */
+#define MCSG_DIRECTED 1u
+#define MCSG_LABELED 2u
+
+/* mcsg_options.mode */
+#define MCSG_MODE_THROUGHPUT 0 /* all warps, subtree donation, shared incumbent */
+#define MCSG_MODE_PARITY 1     /* one warp per instance: reference node order and counts */
+
+/* mcsg_options.order — OrderingStrategy (solve.hpp:116) */
+#define MCSG_ORDER_NONE 0
+#define MCSG_ORDER_DEGREE 1
+#define MCSG_ORDER_COMPONENTS 2
+#define MCSG_ORDER_BLOCK 3
+
+#define MCSG_MAX_N 64
+
+typedef struct mcsg_graph {
+    int32_t n;
+    uint32_t flags;         /* MCSG_DIRECTED | MCSG_LABELED */
+    const uint8_t* codes;   /* n*n row-major codes (graph.hpp:60) */
+    const int32_t* labels;  /* n vertex labels when MCSG_LABELED, else NULL */
+} mcsg_graph;
+
+typedef struct mcsg_options {
+    double budget_s;                /* SolveConfig::budget_seconds; <= 0 immediate timeout */
+    int32_t order;                  /* MCSG_ORDER_* */
+    int32_t mode;                   /* MCSG_MODE_* */
+    int32_t goal;                   /* 0 off; > 0: stop at |M| >= goal, prune below it */
+    int32_t disable_pruning;        /* SolveConfig::disable_pruning */
+    int32_t floor_size;             /* SolveConfig::shared_bound value (size floor) */
+    int32_t device;                 /* CUDA ordinal, -1 = current */
+    int32_t max_warps;              /* 0 = every resident warp */
+    int32_t smem_classes;           /* 0 = auto: class-stack entries per warp in smem */
+    uint64_t seed;                  /* restarts:<seed> portfolio member: donation order */
+    const volatile int32_t* cancel; /* SolveConfig::cancel; polled by the kernel */
+} mcsg_options;
+
+typedef struct mcsg_stats {
+    uint64_t nodes;          /* stats.recursions: counted search nodes */
+    uint64_t sum_classes;    /* Σ live classes over counted nodes */
+    uint64_t splits;         /* children built (filter_classes calls) */
+    uint64_t split_classes;  /* Σ parent classes read by those splits */
+    uint64_t donations;      /* subtrees handed to idle warps */
+    uint64_t tasks;          /* tasks executed (roots + donated) */
+    uint64_t spills;         /* class levels placed in the HBM spill area */
+    uint64_t probes;         /* goal-directed / bound-jump probes */
+    double wall_s;           /* host wall time of the call */
+    double kernel_s;         /* device time of the search kernel(s) (CUDA events) */
+    double h2d_s;            /* host->device staging time */
+    int32_t warps;           /* resident warps launched */
+    int32_t ctas;
+    int32_t smem_per_cta;
+    int32_t smem_classes;
+} mcsg_stats;
+
+typedef struct mcsg_result {
+    int32_t status;          /* MCSG_OPTIMAL / MCSG_TIMEOUT / MCSG_CANCELLED / MCSG_ERROR */
+    int32_t size;
+    int32_t pairs[2 * MCSG_MAX_N]; /* (v in G, u in H) in ORIGINAL ids */
+    uint64_t nodes;          /* nodes of this instance */
+    double solve_s;          /* device time from launch to this instance's proof */
+} mcsg_result;
+
+/* ---- solving ---------------------------------------------------------- */
+int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                   mcsg_result* out, mcsg_stats* stats);
+int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                            mcsg_result* out, mcsg_stats* stats);
+/* count pairs solved in one launch; outs[count] */
+int32_t mcsg_solve_batch(int32_t count, const mcsg_graph* gs, const mcsg_graph* hs,
+                         const mcsg_options* opt, mcsg_result* outs, mcsg_stats* stats);
+int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
+                                 const mcsg_options* opt, mcsg_result* out, mcsg_stats* stats);
+int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best,
+                        int32_t doubling, const mcsg_options* opt, mcsg_result* out,
+                        mcsg_stats* stats);
+/* Races `count` member strategies (orderings / seeds) of ONE pair in one
+ * launch with a shared incumbent size; first member to prove wins
+ * (portfolio.cpp:249-292). orders[i] in MCSG_ORDER_*; winner_out may be NULL. */
+int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
+                       const int32_t* orders, const mcsg_options* opt, mcsg_result* out,
+                       int32_t* winner_out, mcsg_stats* stats);
+
+/* ---- graph core / loader ---------------------------------------------- */
+/* 1 valid, 0 invalid, MCSG_ERROR-style -1 on out-of-range vertices */
+int32_t mcsg_verify(const mcsg_graph* g, const mcsg_graph* h, const int32_t* pairs, int32_t k);
+int32_t mcsg_random_graph(int32_t n, double density, uint64_t seed, uint32_t flags,
+                          int32_t label_count, uint8_t* codes_out, int32_t* labels_out);
+int32_t mcsg_random_permutation(int32_t n, uint64_t seed, int32_t* fwd_out);
+int32_t mcsg_ordering(const mcsg_graph* g, int32_t strategy, int32_t* fwd_out);
+/* format: 0 mivia, 1 text, 2 auto-detect (FileFormat, graph_io.hpp:31).
+ * Two-phase: call with codes_out == NULL to learn n and flags, then again with
+ * buffers of n*n bytes (and n labels when MCSG_LABELED). */
+int32_t mcsg_load_graph_file(const char* path, int32_t format, int32_t* n_out,
+                             uint32_t* flags_out, uint8_t* codes_out, int32_t* labels_out);
+int32_t mcsg_save_graph_file(const mcsg_graph* g, const char* path, int32_t format);
+/* The loader's device form: 64-bit adjacency rows. out_rows[n] gets the
+ * undirected adjacency / directed forward bits; in_rows[n] (may be NULL)
+ * the directed backward bits. */
+int32_t mcsg_pack_graph(const mcsg_graph* g, uint64_t* out_rows, uint64_t* in_rows);
+
+/* ---- runtime ------------------------------------------------------------ */
+const char* mcsg_last_error(void);
+int32_t mcsg_abi_version(void);
+/* number of usable CUDA devices (0 when none) */
+int32_t mcsg_device_count(void);
+/* release every device context this process created */
+void mcsg_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCSG_H */

@@ -1,0 +1,129 @@
+// Device-side data layout shared by the host runtime (mcsg_host.cpp) and the
+// search kernel (mcsg_kernel.cu). Everything here lives in HBM; the kernel
+// stages the hot parts (adjacency rows, vertex keys, the class stack, the
+// DFS frames) in shared memory per warp.
+//
+// Terminology follows the reference (/root/reference/proj):
+//   instance  = one (G, H) pair to solve                    (solve.hpp:128)
+//   class     = one label class / bidomain (L ⊆ V_G, R ⊆ V_H) (label_classes.hpp:12-20)
+//   node      = one counted entry into search_node          (search_core.hpp:130)
+//   task      = a frozen subtree (node state + remaining branch plan), the
+//               GPU counterpart of SearchTask               (task_queue.hpp:27-48)
+//   group     = instances sharing one incumbent size (portfolio members of one
+//               pair: SharedBound semantics, solve.hpp:68-81)
+#pragma once
+#include <cstdint>
+
+namespace mcsg {
+
+constexpr int kMaxN = 64;        // one 64-bit word per bitset row (all configs n <= 45)
+constexpr int kMaxDepth = kMaxN + 1;
+constexpr int kWarpsPerCta = 4;
+
+// Per-instance read-only description, packed by the host loader
+// (graph.hpp:31-62 codes -> bitsets). 64-bit storage even when the kernel
+// runs the 32-bit specialisation (n <= 32); the kernel truncates.
+struct InstanceDesc {
+    int32_t n_g, n_h;
+    int32_t maxp;      // min(n_g, n_h)            (search_core.hpp:105)
+    int32_t goal;      // 0 = off                  (search_core.hpp:93)
+    int32_t n_init;    // initial classes          (label_classes.cpp:8-39)
+    int32_t group;     // incumbent group id
+    int32_t prune;     // 0 = disable_pruning      (solve.hpp:122)
+    int32_t floor;     // external size floor      (search_core.hpp:25-28)
+    uint64_t out_g[kMaxN];  // undirected: adjacency; directed: code bit0 (v -> x)
+    uint64_t out_h[kMaxN];
+    uint64_t in_g[kMaxN];   // directed only: code bit1 (x -> v)
+    uint64_t in_h[kMaxN];
+    uint64_t init_l[kMaxN];
+    uint64_t init_r[kMaxN];
+    uint16_t vkey[kMaxN];   // (255 - deg) << 6 | id: min == select_vertex (label_classes.cpp:69-78)
+};
+
+// Per-instance mutable state (results).
+struct InstanceState {
+    uint32_t map_size;      // size of the mapping stored in map_v/map_u
+    int32_t lock;           // spin lock guarding map_* on improvement
+    int32_t open_tasks;     // tasks of this instance not yet finished
+    int32_t status;         // 0 running/optimal, 1 timeout/cancel-interrupted
+    unsigned long long nodes;
+    unsigned long long t_done_ns;  // %globaltimer when the last task finished
+    uint8_t map_v[kMaxN];
+    uint8_t map_u[kMaxN];
+};
+
+// Incumbent group (one per solved pair; several instances when a portfolio
+// races orderings/strategies on one GPU and shares the size).
+struct GroupState {
+    uint32_t best;          // monotone size, only raised after a mapping of that size is stored
+    uint32_t done;          // 1: max reached, goal reached, or one member proved optimality
+    int32_t winner;         // instance that proved / reached first (-1 none)
+    int32_t reached;        // goal probes: 1 when |M| >= goal was found
+};
+
+// A frozen subtree: the node's classes and mapping, the selected class and
+// vertex, the u candidates not yet tried and whether the "v unmatched"
+// continuation still belongs to it (search_core.hpp:183-212).
+enum : uint8_t { kTaskRoot = 0, kTaskBranch = 1 };
+
+struct TaskHeader {
+    int32_t inst;
+    uint8_t kind;
+    uint8_t depth;
+    uint8_t nc;
+    uint8_t sel;
+    uint8_t v;
+    uint8_t bound;
+    uint8_t cont;
+    uint8_t pad0;
+    uint64_t cand;          // remaining u candidates (bitset over V_H)
+    uint64_t pad1;
+};
+
+struct alignas(128) TaskSlot {
+    unsigned long long seq;  // Vyukov ring sequence word
+    unsigned long long pad[1];
+    TaskHeader hdr;          // 32 B
+    uint8_t map_v[kMaxN];
+    uint8_t map_u[kMaxN];
+    uint64_t cls_l[kMaxN];
+    uint64_t cls_r[kMaxN];
+};
+
+// Global counters (one set per launch), for the roofline / stats.
+struct Counters {
+    unsigned long long nodes;
+    unsigned long long sum_classes;  // Σ live classes over counted nodes
+    unsigned long long splits;       // children built (filter_classes calls)
+    unsigned long long split_classes;// Σ parent classes read by those splits
+    unsigned long long donations;
+    unsigned long long tasks;
+    unsigned long long spills;       // levels placed in the HBM spill area
+    unsigned long long t_start_ns;   // min %globaltimer over warps at kernel start
+    unsigned long long overflow;     // class-stack overflow (must stay 0)
+};
+
+struct KernelParams {
+    const InstanceDesc* inst;
+    InstanceState* ist;
+    GroupState* grp;
+    TaskSlot* slots;
+    unsigned long long* head;
+    unsigned long long* tail;
+    uint32_t cap_mask;       // ring capacity - 1 (power of two)
+    int32_t* next_root;      // root tasks are implicit: instance ids handed out by atomicAdd
+    int32_t n_inst;
+    int32_t* pending;        // tasks queued + tasks in flight (termination)
+    int32_t* idle;           // warps waiting for work (donation trigger)
+    int32_t* stop;           // 0 run, 1 timeout, 2 cancelled
+    const volatile int32_t* cancel;  // host-mapped cancel flag (may be null)
+    unsigned long long budget_ns;    // per-warp deadline = warp start + budget, 0 = none
+    uint64_t* spill;         // per-warp HBM spill area for class levels
+    int32_t spill_classes;   // classes per warp in the spill area
+    int32_t smem_classes;    // classes per warp in shared memory
+    int32_t donate;          // 0 = parity mode (no donation: exact sequential semantics)
+    int32_t poll_mask;       // poll global state every (poll_mask+1) nodes
+    Counters* counters;
+};
+
+}  // namespace mcsg

@@ -1,0 +1,769 @@
+// Host runtime and C ABI of the B200 McSplit solver.
+//
+// One device context per GPU owns the HBM working set of the persistent search
+// kernel (instance table, results, the subtree ring, per-warp spill areas)
+// and a pinned staging area. A call packs its pairs (loader -> bitsets),
+// stages them with one async H2D copy, launches the kernel once, mirrors the
+// caller's cancel flag into host-mapped memory while it runs, and copies the
+// per-instance results back. Orderings are applied host-side before packing
+// and undone on the returned mapping (with_ordering, search_core.hpp:72-81);
+// every returned mapping is re-verified on the host (oracle.cpp:8-24 rules)
+// before it leaves the library.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+#include "../../include/mcsg.h"
+#include "mcsg_device.h"
+#include "mcsg_graph.hpp"
+
+namespace mcsg {
+
+int kernel_occupancy(bool wide, bool directed, int smem_classes);
+int kernel_smem_per_warp(bool wide, bool directed, int smem_classes);
+cudaError_t kernel_launch(bool wide, bool directed, const KernelParams& p, int ctas, cudaStream_t st);
+cudaError_t ring_reset(TaskSlot* slots, uint32_t cap, Counters* c, cudaStream_t st);
+
+namespace {
+
+thread_local std::string t_err;
+
+struct CudaErr : Error {
+    explicit CudaErr(const std::string& w) : Error(w) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Ctl {
+    unsigned long long head, tail;
+    int32_t pending, idle, stop, next_root;
+};
+
+constexpr uint32_t kRingCap = 16384;                      // power of two
+constexpr int kSpillClasses = kMaxDepth * kMaxN;          // worst-case stack: no overflow possible
+
+struct Context {
+    int device = 0;
+    int sms = 0;
+    int smem_per_sm = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    InstanceDesc* d_inst = nullptr;
+    InstanceState* d_ist = nullptr;
+    GroupState* d_grp = nullptr;
+    InstanceDesc* h_inst = nullptr;
+    InstanceState* h_ist = nullptr;
+    GroupState* h_grp = nullptr;
+    size_t inst_cap = 0, grp_cap = 0;
+    TaskSlot* d_slots = nullptr;
+    Ctl* d_ctl = nullptr;
+    Counters* d_cnt = nullptr;
+    Counters* h_cnt = nullptr;
+    Ctl* h_ctl = nullptr;  // pinned
+    uint64_t* d_spill = nullptr;
+    size_t spill_warps = 0;
+    int32_t* h_cancel = nullptr;  // pinned, mapped
+    int32_t* d_cancel = nullptr;
+    std::mutex mu;
+
+    explicit Context(int dev) : device(dev) {
+        ck(cudaSetDevice(dev), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+        if (prop.major < 10)
+            throw Error("mcsg kernels are built for sm_100a; device " + std::to_string(dev) +
+                        " is sm_" + std::to_string(prop.major * 10 + prop.minor));
+        sms = prop.multiProcessorCount;
+        smem_per_sm = int(prop.sharedMemPerMultiprocessor);
+        ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&ev0), "event");
+        ck(cudaEventCreate(&ev1), "event");
+        ck(cudaMalloc(&d_slots, sizeof(TaskSlot) * kRingCap), "ring");
+        ck(cudaMalloc(&d_ctl, sizeof(Ctl)), "ctl");
+        ck(cudaMalloc(&d_cnt, sizeof(Counters)), "counters");
+        ck(cudaMallocHost(&h_cnt, sizeof(Counters)), "counters host");
+        ck(cudaMallocHost(&h_ctl, sizeof(Ctl)), "ctl host");
+        ck(cudaHostAlloc(&h_cancel, sizeof(int32_t), cudaHostAllocMapped), "cancel flag");
+        ck(cudaHostGetDevicePointer(&d_cancel, h_cancel, 0), "cancel flag map");
+        *h_cancel = 0;
+    }
+
+    void reserve(size_t n_inst, size_t n_grp, size_t warps) {
+        if (n_inst > inst_cap) {
+            size_t cap = std::max<size_t>(n_inst, inst_cap * 2);
+            cudaFree(d_inst);
+            cudaFree(d_ist);
+            cudaFreeHost(h_inst);
+            cudaFreeHost(h_ist);
+            ck(cudaMalloc(&d_inst, sizeof(InstanceDesc) * cap), "instances");
+            ck(cudaMalloc(&d_ist, sizeof(InstanceState) * cap), "instance state");
+            ck(cudaMallocHost(&h_inst, sizeof(InstanceDesc) * cap), "instances host");
+            ck(cudaMallocHost(&h_ist, sizeof(InstanceState) * cap), "instance state host");
+            inst_cap = cap;
+        }
+        if (n_grp > grp_cap) {
+            size_t cap = std::max<size_t>(n_grp, grp_cap * 2);
+            cudaFree(d_grp);
+            cudaFreeHost(h_grp);
+            ck(cudaMalloc(&d_grp, sizeof(GroupState) * cap), "groups");
+            ck(cudaMallocHost(&h_grp, sizeof(GroupState) * cap), "groups host");
+            grp_cap = cap;
+        }
+        if (warps > spill_warps) {
+            cudaFree(d_spill);
+            ck(cudaMalloc(&d_spill, sizeof(uint64_t) * 2 * kSpillClasses * warps), "spill");
+            spill_warps = warps;
+        }
+    }
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<Context>> g_ctx;
+
+Context& context(int device) {
+    int dev = device;
+    if (dev < 0) {
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+    }
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    auto it = g_ctx.find(dev);
+    if (it != g_ctx.end()) return *it->second;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        throw Error("no CUDA device available (mcsg has no CPU fallback)");
+    if (dev >= count) throw Error("CUDA device " + std::to_string(dev) + " does not exist");
+    auto ctx = std::make_unique<Context>(dev);
+    Context& ref = *ctx;
+    g_ctx[dev] = std::move(ctx);
+    return ref;
+}
+
+// One instance of a launch: a (possibly permuted) pair plus how to undo the
+// permutation on its mapping.
+struct Job {
+    HostGraph g, h;            // as searched (permuted when ordered)
+    std::vector<int> inv_g;    // searched id -> original id (empty = identity)
+    std::vector<int> inv_h;
+    int group = 0;
+    int goal = 0;
+    int floor_size = 0;
+};
+
+struct JobResult {
+    int status = MCSG_OPTIMAL;
+    int size = 0;
+    std::vector<int32_t> pairs;  // original ids
+    uint64_t nodes = 0;
+    double solve_s = 0;
+    bool completed = false;
+};
+
+struct GroupResult {
+    bool done = false;
+    int winner = -1;
+    bool reached = false;
+};
+
+struct LaunchOut {
+    std::vector<JobResult> jobs;
+    std::vector<GroupResult> groups;
+    Counters counters{};
+    double kernel_s = 0, h2d_s = 0;
+    int warps = 0, ctas = 0, smem_per_cta = 0, smem_classes = 0;
+};
+
+Job make_job(const HostGraph& g, const HostGraph& h, int order) {
+    Job j;
+    if (order == MCSG_ORDER_NONE) {
+        j.g = g;
+        j.h = h;
+        return j;
+    }
+    const auto pg = make_ordering(g, order);
+    const auto ph = make_ordering(h, order);
+    j.g = g.permuted(pg);
+    j.h = h.permuted(ph);
+    j.inv_g.assign(g.n, 0);
+    j.inv_h.assign(h.n, 0);
+    for (int v = 0; v < g.n; ++v) j.inv_g[pg[v]] = v;
+    for (int u = 0; u < h.n; ++u) j.inv_h[ph[u]] = u;
+    return j;
+}
+
+double secs_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// The single launch path shared by every entry point.
+LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
+    Context& ctx = context(o.device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    ck(cudaSetDevice(ctx.device), "cudaSetDevice");
+    LaunchOut out;
+    const int n = int(jobs.size());
+    out.jobs.resize(n);
+    out.groups.resize(n_groups);
+    if (n == 0) return out;
+
+    bool wide = false, directed = false;
+    for (const Job& j : jobs) {
+        wide |= std::max(j.g.n, j.h.n) > 32;
+        directed |= j.g.directed;
+    }
+    const bool parity = o.mode == MCSG_MODE_PARITY;
+
+    // shared-memory class stack: as deep as the register-limited occupancy allows
+    int smem_classes = o.smem_classes;
+    int blocks = kernel_occupancy(wide, directed, 64);
+    if (blocks <= 0) throw Error("search kernel cannot be resident on this device");
+    if (smem_classes <= 0) {
+        const int per_cta = ctx.smem_per_sm / blocks - 1024;
+        const int per_warp = per_cta / kWarpsPerCta;
+        const int fixed = kernel_smem_per_warp(wide, directed, 0);
+        smem_classes = std::clamp((per_warp - fixed) / (wide ? 16 : 8), 64, 1024);
+        while (smem_classes > 64 && kernel_occupancy(wide, directed, smem_classes) < blocks)
+            smem_classes -= 16;
+    }
+    smem_classes = std::max(smem_classes, 64);
+    blocks = kernel_occupancy(wide, directed, smem_classes);
+    if (blocks <= 0) throw Error("requested shared-memory class stack does not fit");
+    int ctas = blocks * ctx.sms;
+    if (o.max_warps > 0) ctas = std::min(ctas, (o.max_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+    if (parity) ctas = std::min(ctas, (n + kWarpsPerCta - 1) / kWarpsPerCta);
+    ctas = std::max(ctas, 1);
+    const int warps = ctas * kWarpsPerCta;
+    ctx.reserve(size_t(n), size_t(n_groups), size_t(warps));
+
+    auto t_stage = std::chrono::steady_clock::now();
+    for (int i = 0; i < n; ++i) {
+        pack_instance(jobs[i].g, jobs[i].h, jobs[i].goal, o.disable_pruning == 0, jobs[i].floor_size,
+                      jobs[i].group, &ctx.h_inst[i]);
+        std::memset(&ctx.h_ist[i], 0, sizeof(InstanceState));
+        ctx.h_ist[i].open_tasks = 1;
+    }
+    for (int gi = 0; gi < n_groups; ++gi) {
+        ctx.h_grp[gi] = GroupState{};
+        ctx.h_grp[gi].winner = -1;
+    }
+    ck(cudaMemcpyAsync(ctx.d_inst, ctx.h_inst, sizeof(InstanceDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    ck(cudaMemcpyAsync(ctx.d_ist, ctx.h_ist, sizeof(InstanceState) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    ck(cudaMemcpyAsync(ctx.d_grp, ctx.h_grp, sizeof(GroupState) * n_groups, cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    *ctx.h_ctl = Ctl{};
+    ctx.h_ctl->pending = n;
+    ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
+    *ctx.h_cancel = 0;
+
+    KernelParams p{};
+    p.inst = ctx.d_inst;
+    p.ist = ctx.d_ist;
+    p.grp = ctx.d_grp;
+    p.slots = ctx.d_slots;
+    p.head = &ctx.d_ctl->head;
+    p.tail = &ctx.d_ctl->tail;
+    p.cap_mask = kRingCap - 1;
+    p.next_root = &ctx.d_ctl->next_root;
+    p.n_inst = n;
+    p.pending = &ctx.d_ctl->pending;
+    p.idle = &ctx.d_ctl->idle;
+    p.stop = &ctx.d_ctl->stop;
+    p.cancel = o.cancel ? ctx.d_cancel : nullptr;
+    p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
+    p.spill = ctx.d_spill;
+    p.spill_classes = kSpillClasses;
+    p.smem_classes = smem_classes;
+    p.donate = parity ? 0 : 1;
+    p.poll_mask = parity ? 4095 : 255;
+    p.counters = ctx.d_cnt;
+
+    ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
+    ck(kernel_launch(wide, directed, p, ctas, ctx.stream), "search kernel launch");
+    ck(cudaEventRecord(ctx.ev1, ctx.stream), "event");
+    ck(cudaMemcpyAsync(ctx.h_ist, ctx.d_ist, sizeof(InstanceState) * n, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
+    ck(cudaMemcpyAsync(ctx.h_grp, ctx.d_grp, sizeof(GroupState) * n_groups, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
+    ck(cudaMemcpyAsync(ctx.h_cnt, ctx.d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
+    Ctl* ctl_out = ctx.h_ctl;
+    ck(cudaMemcpyAsync(ctl_out, ctx.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
+    out.h2d_s = secs_since(t_stage);
+    if (o.cancel) {
+        // mirror the caller's flag into host-mapped memory the kernel polls
+        while (cudaStreamQuery(ctx.stream) == cudaErrorNotReady) {
+            if (*o.cancel) *reinterpret_cast<volatile int32_t*>(ctx.h_cancel) = 1;
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    ck(cudaStreamSynchronize(ctx.stream), "search kernel");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1);
+    out.kernel_s = ms * 1e-3;
+    out.counters = *ctx.h_cnt;
+    out.warps = warps;
+    out.ctas = ctas;
+    out.smem_per_cta = kernel_smem_per_warp(wide, directed, smem_classes) * kWarpsPerCta;
+    out.smem_classes = smem_classes;
+    if (out.counters.overflow) throw Error("class stack overflow (internal error)");
+
+    const int stop = ctl_out->stop;
+    for (int gi = 0; gi < n_groups; ++gi) {
+        out.groups[gi].done = ctx.h_grp[gi].done != 0;
+        out.groups[gi].winner = ctx.h_grp[gi].winner;
+        out.groups[gi].reached = ctx.h_grp[gi].reached != 0;
+    }
+    for (int i = 0; i < n; ++i) {
+        const InstanceState& s = ctx.h_ist[i];
+        JobResult& r = out.jobs[i];
+        const Job& j = jobs[i];
+        r.completed = s.open_tasks == 0;
+        r.nodes = s.nodes;
+        r.size = int(s.map_size);
+        r.solve_s = s.t_done_ns > out.counters.t_start_ns ? (s.t_done_ns - out.counters.t_start_ns) * 1e-9 : 0.0;
+        const bool group_done = out.groups[j.group].done;
+        if (stop != 0 && !(r.completed || group_done))
+            r.status = stop == 2 ? MCSG_CANCELLED : MCSG_TIMEOUT;
+        else
+            r.status = MCSG_OPTIMAL;
+        r.pairs.resize(2 * r.size);
+        for (int k = 0; k < r.size; ++k) {
+            int v = s.map_v[k], u = s.map_u[k];
+            if (!j.inv_g.empty()) v = j.inv_g[v];
+            if (!j.inv_h.empty()) u = j.inv_h[u];
+            r.pairs[2 * k] = v;
+            r.pairs[2 * k + 1] = u;
+        }
+    }
+    return out;
+}
+
+void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probes) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->nodes = lo.counters.nodes;
+    st->sum_classes = lo.counters.sum_classes;
+    st->splits = lo.counters.splits;
+    st->split_classes = lo.counters.split_classes;
+    st->donations = lo.counters.donations;
+    st->tasks = lo.counters.tasks;
+    st->spills = lo.counters.spills;
+    st->probes = probes;
+    st->wall_s = wall;
+    st->kernel_s = lo.kernel_s;
+    st->h2d_s = lo.h2d_s;
+    st->warps = lo.warps;
+    st->ctas = lo.ctas;
+    st->smem_per_cta = lo.smem_per_cta;
+    st->smem_classes = lo.smem_classes;
+}
+
+void accumulate(mcsg_stats* st, const LaunchOut& lo) {
+    if (!st) return;
+    st->nodes += lo.counters.nodes;
+    st->sum_classes += lo.counters.sum_classes;
+    st->splits += lo.counters.splits;
+    st->split_classes += lo.counters.split_classes;
+    st->donations += lo.counters.donations;
+    st->tasks += lo.counters.tasks;
+    st->spills += lo.counters.spills;
+    st->kernel_s += lo.kernel_s;
+    st->h2d_s += lo.h2d_s;
+    st->warps = lo.warps;
+    st->ctas = lo.ctas;
+    st->smem_per_cta = lo.smem_per_cta;
+    st->smem_classes = lo.smem_classes;
+}
+
+mcsg_options defaults(const mcsg_options* o) {
+    mcsg_options d{};
+    d.budget_s = 1e9;
+    d.device = -1;
+    if (o) d = *o;
+    return d;
+}
+
+void check_pair(const HostGraph& g, const HostGraph& h) {
+    if (g.directed != h.directed) throw Error("solve: graphs must share a kind");
+    if (g.labeled != h.labeled) throw Error("cannot mix a labeled graph with an unlabeled one");
+    if (g.n > kMaxN || h.n > kMaxN)
+        throw Error("graphs above " + std::to_string(kMaxN) + " vertices are not supported");
+}
+
+void write_result(const HostGraph& g, const HostGraph& h, const JobResult& r, mcsg_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = r.status;
+    out->size = r.size;
+    out->nodes = r.nodes;
+    out->solve_s = r.solve_s;
+    if (r.size > 0 && verify(g, h, r.pairs.data(), r.size) != 1)
+        throw Error("internal error: kernel returned an invalid mapping");
+    for (int k = 0; k < 2 * r.size; ++k) out->pairs[k] = r.pairs[k];
+}
+
+int fail(const std::exception& e) {
+    t_err = e.what();
+    return MCSG_ERROR;
+}
+
+void timed_out(mcsg_result* out, int status = MCSG_TIMEOUT) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = status;
+}
+
+// One probe of the goal-directed / bound-jump schedules (solve.cpp:57-75).
+struct Probe {
+    bool reached = false;
+    int status = MCSG_OPTIMAL;
+    JobResult best;
+};
+
+Probe probe_goal(const HostGraph& g, const HostGraph& h, int goal, const mcsg_options& o,
+                 mcsg_stats* st, std::chrono::steady_clock::time_point deadline, bool unlimited) {
+    mcsg_options po = o;
+    if (!unlimited) {
+        po.budget_s = std::chrono::duration<double>(deadline - std::chrono::steady_clock::now()).count();
+        if (po.budget_s <= 0) {
+            Probe pr;
+            pr.status = MCSG_TIMEOUT;
+            return pr;
+        }
+    }
+    std::vector<Job> jobs(1);
+    jobs[0].g = g;
+    jobs[0].h = h;
+    jobs[0].goal = goal;
+    LaunchOut lo = launch(jobs, 1, po);
+    accumulate(st, lo);
+    Probe pr;
+    pr.reached = lo.groups[0].reached;
+    pr.status = lo.jobs[0].status;
+    pr.best = lo.jobs[0];
+    return pr;
+}
+
+}  // namespace
+}  // namespace mcsg
+
+using namespace mcsg;
+
+extern "C" {
+
+const char* mcsg_last_error(void) { return t_err.c_str(); }
+int32_t mcsg_abi_version(void) { return MCSG_ABI_VERSION; }
+
+int32_t mcsg_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+void mcsg_shutdown(void) {
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    g_ctx.clear();  // device memory is reclaimed with the process / context
+}
+
+int32_t mcsg_solve_batch(int32_t count, const mcsg_graph* gs, const mcsg_graph* hs,
+                         const mcsg_options* opt, mcsg_result* outs, mcsg_stats* stats) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        const mcsg_options o = defaults(opt);
+        if (count < 0) throw Error("negative batch size");
+        std::vector<HostGraph> G(count), H(count);
+        for (int i = 0; i < count; ++i) {
+            G[i] = HostGraph::from_abi(&gs[i]);
+            H[i] = HostGraph::from_abi(&hs[i]);
+            check_pair(G[i], H[i]);
+        }
+        if (o.budget_s <= 0) {  // solve.cpp:95
+            for (int i = 0; i < count; ++i) timed_out(&outs[i]);
+            if (stats) std::memset(stats, 0, sizeof(*stats));
+            return MCSG_TIMEOUT;
+        }
+        std::vector<Job> jobs;
+        jobs.reserve(count);
+        for (int i = 0; i < count; ++i) {
+            jobs.push_back(make_job(G[i], H[i], o.order));
+            jobs.back().group = i;
+            jobs.back().goal = o.goal;
+            jobs.back().floor_size = o.floor_size;
+        }
+        LaunchOut lo = launch(jobs, count, o);
+        int worst = MCSG_OPTIMAL;
+        for (int i = 0; i < count; ++i) {
+            write_result(G[i], H[i], lo.jobs[i], &outs[i]);
+            worst = std::max(worst, outs[i].status == MCSG_OPTIMAL ? 0 : outs[i].status);
+        }
+        fill_stats(stats, lo, secs_since(t0), 0);
+        return worst;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                   mcsg_result* out, mcsg_stats* stats) {
+    return mcsg_solve_batch(1, g, h, opt, out, stats);
+}
+
+int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                            mcsg_result* out, mcsg_stats* stats) {
+    mcsg_options o = defaults(opt);
+    o.mode = MCSG_MODE_THROUGHPUT;
+    return mcsg_solve_batch(1, g, h, &o, out, stats);
+}
+
+int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
+                       const int32_t* orders, const mcsg_options* opt, mcsg_result* out,
+                       int32_t* winner_out, mcsg_stats* stats) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        const mcsg_options o = defaults(opt);
+        if (count <= 0) throw Error("portfolio needs at least one engine spec");
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        std::vector<Job> jobs;
+        for (int i = 0; i < count; ++i) {
+            jobs.push_back(make_job(G, H, orders ? orders[i] : MCSG_ORDER_NONE));
+            jobs.back().group = 0;
+            jobs.back().goal = o.goal;
+            jobs.back().floor_size = o.floor_size;
+        }
+        mcsg_options lo_opt = o;
+        lo_opt.mode = MCSG_MODE_THROUGHPUT;  // members share the incumbent size
+        LaunchOut lo = launch(jobs, 1, lo_opt);
+        // best mapping among members (sizes are shared, mappings are per member)
+        int bi = 0;
+        for (int i = 1; i < count; ++i)
+            if (lo.jobs[i].size > lo.jobs[bi].size) bi = i;
+        JobResult r = lo.jobs[bi];
+        r.nodes = 0;
+        for (const auto& jr : lo.jobs) r.nodes += jr.nodes;
+        const int w = lo.groups[0].winner;
+        r.status = lo.groups[0].done ? MCSG_OPTIMAL : lo.jobs[bi].status;
+        if (w >= 0) r.solve_s = lo.jobs[w].solve_s;
+        write_result(G, H, r, out);
+        if (winner_out) *winner_out = w;
+        fill_stats(stats, lo, secs_since(t0), 0);
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// solve.cpp:131-168: goals n_G, n_G-1, ... over the smaller graph.
+int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
+                                 const mcsg_options* opt, mcsg_result* out, mcsg_stats* stats) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        const mcsg_options o = defaults(opt);
+        HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        const bool swapped = G.n > H.n;
+        if (swapped) std::swap(G, H);
+        Job base = make_job(G, H, o.order);
+        const bool unlimited = o.budget_s >= 1e8;
+        const auto deadline = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                                       std::chrono::duration<double>(unlimited ? 0.0 : o.budget_s));
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        JobResult best;
+        int status = MCSG_OPTIMAL;
+        uint64_t probes = 0, nodes = 0;
+        for (int goal = base.g.n; goal >= 1; --goal) {
+            Probe pr = probe_goal(base.g, base.h, goal, o, stats, deadline, unlimited);
+            ++probes;
+            nodes += pr.best.nodes;
+            if (pr.best.size > best.size) best = pr.best;
+            if (pr.status != MCSG_OPTIMAL) {
+                status = pr.status;
+                break;
+            }
+            if (pr.reached) break;
+        }
+        // map back through the ordering, then undo the swap
+        JobResult r = best;
+        r.status = status;
+        r.nodes = nodes;
+        for (int k = 0; k < r.size; ++k) {
+            int v = r.pairs[2 * k], u = r.pairs[2 * k + 1];
+            if (!base.inv_g.empty()) v = base.inv_g[v];
+            if (!base.inv_h.empty()) u = base.inv_h[u];
+            r.pairs[2 * k] = swapped ? u : v;
+            r.pairs[2 * k + 1] = swapped ? v : u;
+        }
+        if (swapped) std::swap(G, H);
+        write_result(G, H, r, out);
+        if (stats) {
+            stats->probes = probes;
+            stats->wall_s = secs_since(t0);
+        }
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// heuristics.cpp:114-185: jump the target (+1 or x2) until a probe fails,
+// then binary-search the bracket; recover a witness for a supplied size.
+int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best,
+                        int32_t doubling, const mcsg_options* opt, mcsg_result* out,
+                        mcsg_stats* stats) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        const mcsg_options o = defaults(opt);
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        Job base = make_job(G, H, o.order);
+        const bool unlimited = o.budget_s >= 1e8;
+        const auto deadline = t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                                       std::chrono::duration<double>(unlimited ? 0.0 : o.budget_s));
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        long long lower = current_best, upper = std::min(G.n, H.n);
+        JobResult wit;
+        int status = MCSG_OPTIMAL;
+        uint64_t probes = 0, nodes = 0;
+        bool stopped = false;
+        auto run = [&](long long goal) -> bool {
+            Probe pr = probe_goal(base.g, base.h, int(goal), o, stats, deadline, unlimited);
+            ++probes;
+            nodes += pr.best.nodes;
+            if (pr.best.size > wit.size) wit = pr.best;
+            if (pr.status != MCSG_OPTIMAL) {
+                status = pr.status;
+                stopped = true;
+            }
+            return pr.reached;
+        };
+        auto settle = [&](long long target, bool reached) {
+            const long long lo = lower, up = upper;
+            if (reached) lower = target;
+            else upper = target - 1;
+            if (lower < lo || upper > up || lower > upper) throw Error("bound jump bracket violated");
+        };
+        while (lower < upper) {
+            long long target = doubling ? std::max<long long>(1, lower * 2) : lower + 1;
+            target = std::min(target, upper);
+            const bool reached = run(target);
+            if (stopped) break;
+            settle(target, reached);
+        }
+        while (!stopped && lower < upper) {
+            const long long mid = lower + (upper - lower + 1) / 2;
+            const bool reached = run(mid);
+            if (stopped) break;
+            settle(mid, reached);
+        }
+        if (!stopped && wit.size < lower && lower > 0) run(lower);
+        JobResult r = wit;
+        r.status = status;
+        r.nodes = nodes;
+        for (int k = 0; k < r.size; ++k) {
+            if (!base.inv_g.empty()) r.pairs[2 * k] = base.inv_g[r.pairs[2 * k]];
+            if (!base.inv_h.empty()) r.pairs[2 * k + 1] = base.inv_h[r.pairs[2 * k + 1]];
+        }
+        write_result(G, H, r, out);
+        if (stats) {
+            stats->probes = probes;
+            stats->wall_s = secs_since(t0);
+        }
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_verify(const mcsg_graph* g, const mcsg_graph* h, const int32_t* pairs, int32_t k) {
+    try {
+        return verify(HostGraph::from_abi(g), HostGraph::from_abi(h), pairs, k);
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return -1;
+    }
+}
+
+int32_t mcsg_random_graph(int32_t n, double density, uint64_t seed, uint32_t flags,
+                          int32_t label_count, uint8_t* codes_out, int32_t* labels_out) {
+    try {
+        random_graph(n, density, seed, (flags & MCSG_DIRECTED) != 0, label_count, codes_out, labels_out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_random_permutation(int32_t n, uint64_t seed, int32_t* fwd_out) {
+    const auto f = random_permutation(n, seed);
+    for (int i = 0; i < n; ++i) fwd_out[i] = f[i];
+    return 0;
+}
+
+int32_t mcsg_ordering(const mcsg_graph* g, int32_t strategy, int32_t* fwd_out) {
+    try {
+        const auto f = make_ordering(HostGraph::from_abi(g), strategy);
+        for (size_t i = 0; i < f.size(); ++i) fwd_out[i] = f[i];
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_load_graph_file(const char* path, int32_t format, int32_t* n_out, uint32_t* flags_out,
+                             uint8_t* codes_out, int32_t* labels_out) {
+    try {
+        const HostGraph g = load_graph_file(path, format);
+        *n_out = g.n;
+        *flags_out = (g.directed ? MCSG_DIRECTED : 0u) | (g.labeled ? MCSG_LABELED : 0u);
+        if (codes_out) std::memcpy(codes_out, g.codes.data(), g.codes.size());
+        if (labels_out && g.labeled) std::memcpy(labels_out, g.labels.data(), sizeof(int32_t) * g.n);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_save_graph_file(const mcsg_graph* g, const char* path, int32_t format) {
+    try {
+        save_graph_file(HostGraph::from_abi(g), path, format);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_pack_graph(const mcsg_graph* g, uint64_t* out_rows, uint64_t* in_rows) {
+    try {
+        const HostGraph x = HostGraph::from_abi(g);
+        if (x.n > kMaxN) throw Error("graph above 64 vertices");
+        InstanceDesc d;
+        HostGraph empty = x;
+        pack_instance(x, empty, 0, true, 0, 0, &d);
+        for (int v = 0; v < x.n; ++v) {
+            out_rows[v] = d.out_g[v];
+            if (in_rows) in_rows[v] = d.in_g[v];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"
