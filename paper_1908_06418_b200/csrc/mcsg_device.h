@@ -103,26 +103,38 @@ struct Counters {
     unsigned long long overflow;     // class-stack overflow (must stay 0)
 };
 
+// Control words of one launch, one 128-byte line each so that idle warps
+// polling the ring do not contend with busy warps' counters.
+struct alignas(128) Line64 {
+    unsigned long long v;
+};
+struct alignas(128) Line32 {
+    int32_t v;
+};
+struct Ctl {
+    Line64 head;       // ring consumer ticket
+    Line64 tail;       // ring producer ticket
+    Line32 pending;    // tasks queued + tasks in flight (termination)
+    Line32 idle;       // warps waiting for work (donation trigger)
+    Line32 stop;       // 0 run, 1 timeout, 2 cancelled, 3 internal error
+    Line32 next_root;  // root tasks are implicit: instance ids handed out by atomicAdd
+};
+
 struct KernelParams {
     const InstanceDesc* inst;
     InstanceState* ist;
     GroupState* grp;
     TaskSlot* slots;
-    unsigned long long* head;
-    unsigned long long* tail;
+    Ctl* ctl;
     uint32_t cap_mask;       // ring capacity - 1 (power of two)
-    int32_t* next_root;      // root tasks are implicit: instance ids handed out by atomicAdd
     int32_t n_inst;
-    int32_t* pending;        // tasks queued + tasks in flight (termination)
-    int32_t* idle;           // warps waiting for work (donation trigger)
-    int32_t* stop;           // 0 run, 1 timeout, 2 cancelled
     const volatile int32_t* cancel;  // host-mapped cancel flag (may be null)
     unsigned long long budget_ns;    // per-warp deadline = warp start + budget, 0 = none
-    uint64_t* spill;         // per-warp HBM spill area for class levels
+    uint64_t* spill;         // per-warp HBM spill area for class levels (64-bit kernel only)
     int32_t spill_classes;   // classes per warp in the spill area
     int32_t smem_classes;    // classes per warp in shared memory
     int32_t donate;          // 0 = parity mode (no donation: exact sequential semantics)
-    int32_t poll_mask;       // poll global state every (poll_mask+1) nodes
+    int32_t poll_interval;   // poll global state every poll_interval nodes
     Counters* counters;
 };
 

@@ -42,11 +42,6 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-struct Ctl {
-    unsigned long long head, tail;
-    int32_t pending, idle, stop, next_root;
-};
-
 constexpr uint32_t kRingCap = 16384;                      // power of two
 constexpr int kSpillClasses = kMaxDepth * kMaxN;          // worst-case stack: no overflow possible
 
@@ -220,7 +215,13 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     }
     const bool parity = o.mode == MCSG_MODE_PARITY;
 
-    // shared-memory class stack: as deep as the register-limited occupancy allows
+    // Shared-memory class stack. A search level at depth d holds at most
+    // min(n_G, n_H) - d classes, so m(m+1)/2 (+ one level of slack) bounds the
+    // whole path: the 32-bit kernel never spills. The 64-bit kernel takes
+    // what the register-limited occupancy leaves and spills beyond it.
+    int maxm = 0;
+    for (const Job& j : jobs) maxm = std::max(maxm, std::min(j.g.n, j.h.n));
+    const int path_bound = maxm * (maxm + 1) / 2 + 2 * kMaxN;
     int smem_classes = o.smem_classes;
     int blocks = kernel_occupancy(wide, directed, 64);
     if (blocks <= 0) throw Error("search kernel cannot be resident on this device");
@@ -228,7 +229,8 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
         const int per_cta = ctx.smem_per_sm / blocks - 1024;
         const int per_warp = per_cta / kWarpsPerCta;
         const int fixed = kernel_smem_per_warp(wide, directed, 0);
-        smem_classes = std::clamp((per_warp - fixed) / (wide ? 16 : 8), 64, 1024);
+        smem_classes = std::clamp((per_warp - fixed) / (wide ? 16 : 8), 64, 2048);
+        smem_classes = std::min(smem_classes, path_bound);
         while (smem_classes > 64 && kernel_occupancy(wide, directed, smem_classes) < blocks)
             smem_classes -= 16;
     }
@@ -257,7 +259,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     ck(cudaMemcpyAsync(ctx.d_ist, ctx.h_ist, sizeof(InstanceState) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_grp, ctx.h_grp, sizeof(GroupState) * n_groups, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     *ctx.h_ctl = Ctl{};
-    ctx.h_ctl->pending = n;
+    ctx.h_ctl->pending.v = n;
     ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
     *ctx.h_cancel = 0;
@@ -267,21 +269,16 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     p.ist = ctx.d_ist;
     p.grp = ctx.d_grp;
     p.slots = ctx.d_slots;
-    p.head = &ctx.d_ctl->head;
-    p.tail = &ctx.d_ctl->tail;
+    p.ctl = ctx.d_ctl;
     p.cap_mask = kRingCap - 1;
-    p.next_root = &ctx.d_ctl->next_root;
     p.n_inst = n;
-    p.pending = &ctx.d_ctl->pending;
-    p.idle = &ctx.d_ctl->idle;
-    p.stop = &ctx.d_ctl->stop;
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
     p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
     p.spill = ctx.d_spill;
     p.spill_classes = kSpillClasses;
     p.smem_classes = smem_classes;
     p.donate = parity ? 0 : 1;
-    p.poll_mask = parity ? 4095 : 255;
+    p.poll_interval = parity ? 4096 : 256;
     p.counters = ctx.d_cnt;
 
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
@@ -311,7 +308,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     out.smem_classes = smem_classes;
     if (out.counters.overflow) throw Error("class stack overflow (internal error)");
 
-    const int stop = ctl_out->stop;
+    const int stop = ctl_out->stop.v;
     for (int gi = 0; gi < n_groups; ++gi) {
         out.groups[gi].done = ctx.h_grp[gi].done != 0;
         out.groups[gi].winner = ctx.h_grp[gi].winner;
