@@ -101,6 +101,9 @@ typedef struct mcsg_stats {
     int32_t ctas;
     int32_t smem_per_cta;
     int32_t smem_classes;
+    uint64_t h2d_bytes;      /* bytes copied host->device by the call */
+    uint64_t d2h_bytes;      /* bytes copied device->host by the call */
+    uint64_t launches;       /* kernels launched by the call */
 } mcsg_stats;
 
 typedef struct mcsg_result {
@@ -151,6 +154,11 @@ int32_t mcsg_pack_graph(const mcsg_graph* g, uint64_t* out_rows, uint64_t* in_ro
 
 /* ---- runtime ------------------------------------------------------------ */
 const char* mcsg_last_error(void);
+/* class of the last error: GraphError, ParseError (graph_io.hpp:11) or CUDA runtime */
+#define MCSG_ERR_GRAPH 1
+#define MCSG_ERR_PARSE 2
+#define MCSG_ERR_CUDA 3
+int32_t mcsg_last_error_kind(void);
 int32_t mcsg_abi_version(void);
 /* number of usable CUDA devices (0 when none) */
 int32_t mcsg_device_count(void);

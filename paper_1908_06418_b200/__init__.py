@@ -103,7 +103,8 @@ class _Stats(C.Structure):
                 ("split_classes", C.c_uint64), ("donations", C.c_uint64), ("tasks", C.c_uint64),
                 ("spills", C.c_uint64), ("probes", C.c_uint64), ("wall_s", C.c_double),
                 ("kernel_s", C.c_double), ("h2d_s", C.c_double), ("warps", C.c_int32),
-                ("ctas", C.c_int32), ("smem_per_cta", C.c_int32), ("smem_classes", C.c_int32)]
+                ("ctas", C.c_int32), ("smem_per_cta", C.c_int32), ("smem_classes", C.c_int32),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64)]
 
 
 class _Result(C.Structure):
@@ -140,6 +141,7 @@ def lib():
         L.mcsg_save_graph_file.argtypes = [G, C.c_char_p, C.c_int32]
         L.mcsg_pack_graph.argtypes = [G, P(C.c_uint64), P(C.c_uint64)]
         L.mcsg_last_error.restype = C.c_char_p
+        L.mcsg_last_error_kind.restype = C.c_int32
         L.mcsg_abi_version.restype = C.c_int32
         L.mcsg_device_count.restype = C.c_int32
         _lib = L
@@ -148,7 +150,7 @@ def lib():
 
 def _err():
     msg = lib().mcsg_last_error().decode()
-    if "MIVIA" in msg or "text graph" in msg or "cannot open" in msg:
+    if lib().mcsg_last_error_kind() == 2:  # MCSG_ERR_PARSE
         return ParseError(msg)
     return GraphError(msg)
 
@@ -388,6 +390,9 @@ class SearchStats:
     smem_per_cta: int = 0
     smem_classes: int = 0
     h2d_seconds: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    launches: int = 0
 
 
 @dataclass
@@ -434,6 +439,7 @@ def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
         s.sum_classes, s.splits, s.split_classes = int(st.sum_classes), int(st.splits), int(st.split_classes)
         s.donations, s.tasks, s.spills = int(st.donations), int(st.tasks), int(st.spills)
         s.warps, s.ctas, s.smem_per_cta, s.smem_classes = st.warps, st.ctas, st.smem_per_cta, st.smem_classes
+        s.h2d_bytes, s.d2h_bytes, s.launches = int(st.h2d_bytes), int(st.d2h_bytes), int(st.launches)
     return SolveResult(SolveStatus(r.status), pairs, int(r.size), s)
 
 

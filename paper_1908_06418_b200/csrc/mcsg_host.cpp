@@ -33,6 +33,7 @@ cudaError_t ring_reset(TaskSlot* slots, uint32_t cap, Counters* c, cudaStream_t 
 namespace {
 
 thread_local std::string t_err;
+thread_local int t_err_kind = 0;
 
 struct CudaErr : Error {
     explicit CudaErr(const std::string& w) : Error(w) {}
@@ -173,6 +174,7 @@ struct LaunchOut {
     Counters counters{};
     double kernel_s = 0, h2d_s = 0;
     int warps = 0, ctas = 0, smem_per_cta = 0, smem_classes = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
 };
 
 Job make_job(const HostGraph& g, const HostGraph& h, int order) {
@@ -306,6 +308,11 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     out.ctas = ctas;
     out.smem_per_cta = kernel_smem_per_warp(wide, directed, smem_classes) * kWarpsPerCta;
     out.smem_classes = smem_classes;
+    out.h2d_bytes = (sizeof(InstanceDesc) + sizeof(InstanceState)) * uint64_t(n) +
+                    sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl);
+    out.d2h_bytes = sizeof(InstanceState) * uint64_t(n) + sizeof(GroupState) * uint64_t(n_groups) +
+                    sizeof(Counters) + sizeof(Ctl);
+    out.launches = 2;  // ring reset + search kernel
     if (out.counters.overflow) throw Error("class stack overflow (internal error)");
 
     const int stop = ctl_out->stop.v;
@@ -357,6 +364,9 @@ void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probe
     st->ctas = lo.ctas;
     st->smem_per_cta = lo.smem_per_cta;
     st->smem_classes = lo.smem_classes;
+    st->h2d_bytes = lo.h2d_bytes;
+    st->d2h_bytes = lo.d2h_bytes;
+    st->launches = lo.launches;
 }
 
 void accumulate(mcsg_stats* st, const LaunchOut& lo) {
@@ -374,6 +384,9 @@ void accumulate(mcsg_stats* st, const LaunchOut& lo) {
     st->ctas = lo.ctas;
     st->smem_per_cta = lo.smem_per_cta;
     st->smem_classes = lo.smem_classes;
+    st->h2d_bytes += lo.h2d_bytes;
+    st->d2h_bytes += lo.d2h_bytes;
+    st->launches += lo.launches;
 }
 
 mcsg_options defaults(const mcsg_options* o) {
@@ -404,6 +417,9 @@ void write_result(const HostGraph& g, const HostGraph& h, const JobResult& r, mc
 
 int fail(const std::exception& e) {
     t_err = e.what();
+    t_err_kind = dynamic_cast<const ParseErr*>(&e) ? MCSG_ERR_PARSE
+                 : dynamic_cast<const CudaErr*>(&e) ? MCSG_ERR_CUDA
+                                                    : MCSG_ERR_GRAPH;
     return MCSG_ERROR;
 }
 
@@ -451,6 +467,7 @@ using namespace mcsg;
 extern "C" {
 
 const char* mcsg_last_error(void) { return t_err.c_str(); }
+int32_t mcsg_last_error_kind(void) { return t_err_kind; }
 int32_t mcsg_abi_version(void) { return MCSG_ABI_VERSION; }
 
 int32_t mcsg_device_count(void) {
@@ -692,7 +709,7 @@ int32_t mcsg_verify(const mcsg_graph* g, const mcsg_graph* h, const int32_t* pai
     try {
         return verify(HostGraph::from_abi(g), HostGraph::from_abi(h), pairs, k);
     } catch (const std::exception& e) {
-        t_err = e.what();
+        fail(e);
         return -1;
     }
 }
