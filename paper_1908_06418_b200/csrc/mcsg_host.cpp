@@ -27,7 +27,8 @@ namespace mcsg {
 
 int kernel_occupancy(bool wide, bool directed, int smem_classes);
 int kernel_smem_per_warp(bool wide, bool directed, int smem_classes);
-cudaError_t kernel_launch(bool wide, bool directed, const KernelParams& p, int ctas, cudaStream_t st);
+cudaError_t kernel_launch(bool wide, bool directed, bool parity, const KernelParams& p, int ctas,
+                          cudaStream_t st);
 cudaError_t ring_reset(TaskSlot* slots, uint32_t cap, Counters* c, cudaStream_t st);
 
 namespace {
@@ -195,6 +196,25 @@ Job make_job(const HostGraph& g, const HostGraph& h, int order) {
     return j;
 }
 
+// Throughput mode: relabel G so that its ids follow select_vertex's order
+// (degree desc, id asc; label_classes.cpp:69-78). The kernel then picks v with
+// one ctz; the composed permutation is undone on the returned mapping.
+void relabel_for_throughput(Job& j) {
+    const int n = j.g.n;
+    std::vector<int> order(n);
+    for (int v = 0; v < n; ++v) order[v] = v;
+    std::vector<int> deg(n);
+    for (int v = 0; v < n; ++v) deg[v] = j.g.degree(v);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return deg[a] != deg[b] ? deg[a] > deg[b] : a < b; });
+    std::vector<int> fwd(n);
+    for (int pos = 0; pos < n; ++pos) fwd[order[pos]] = pos;
+    std::vector<int> inv(n);
+    for (int v = 0; v < n; ++v) inv[fwd[v]] = j.inv_g.empty() ? v : j.inv_g[v];
+    j.g = j.g.permuted(fwd);
+    j.inv_g = std::move(inv);
+}
+
 double secs_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -216,6 +236,8 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
         directed |= j.g.directed;
     }
     const bool parity = o.mode == MCSG_MODE_PARITY;
+    if (!parity)
+        for (Job& j : jobs) relabel_for_throughput(j);
 
     // Shared-memory class stack. A search level at depth d holds at most
     // min(n_G, n_H) - d classes, so m(m+1)/2 (+ one level of slack) bounds the
@@ -284,7 +306,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     p.counters = ctx.d_cnt;
 
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
-    ck(kernel_launch(wide, directed, p, ctas, ctx.stream), "search kernel launch");
+    ck(kernel_launch(wide, directed, parity, p, ctas, ctx.stream), "search kernel launch");
     ck(cudaEventRecord(ctx.ev1, ctx.stream), "event");
     ck(cudaMemcpyAsync(ctx.h_ist, ctx.d_ist, sizeof(InstanceState) * n, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_grp, ctx.d_grp, sizeof(GroupState) * n_groups, cudaMemcpyDeviceToHost, ctx.stream), "d2h");

@@ -1,334 +1,47 @@
-// McSplit branch-and-bound on sm_100a.
+// The persistent McSplit search kernel (sm_100a) and its launch glue.
 //
-// One warp owns one DFS; lane c holds label class c of the current search
-// level in registers (class = pair of vertex bitsets L ⊆ V_G, R ⊆ V_H); the
-// levels of the current path live in a per-warp shared-memory stack (64-bit
-// kernel: spills to HBM past the shared-memory capacity); subtrees move
-// between warps through a lock-free ring in HBM.
+// Each warp loops: take a task (an instance root from an atomic counter, or a
+// donated subtree from the HBM ring), run its DFS, finish it. The DFS itself:
 //
-// Reference semantics restated (file:line under /root/reference/proj):
-//   node entry / counting         src/search_core.hpp:129-131
-//   incumbent offer + stops       src/search_core.hpp:145-155, src/solve.cpp:19-28
-//   bound (Eq. 1)                 src/label_classes.cpp:41-45
-//   prune test                    src/search_core.hpp:166
-//   select_label_class            src/label_classes.cpp:47-67
-//   select_vertex                 src/label_classes.cpp:69-78
-//   u loop, ascending ids         src/search_core.hpp:183-200
-//   filter_classes (2/4-way)      src/label_classes.cpp:80-108
-//   v-unmatched continuation      src/search_core.hpp:201-212
-//   task queue / delegation       src/task_queue.cpp, src/engine_parallel.cpp:86-117
+//   select  choose the label class (min max(|L|,|R|), label_classes.cpp:47-67)
+//           and the vertex v (max degree, label_classes.cpp:69-78)
+//   next    for each u of the class's right side in ascending id
+//           (search_core.hpp:183-200): count the child node, offer its
+//           mapping when it improves (search_core.hpp:145-155), compute its
+//           bound from the register-resident level (label_classes.cpp:41-45)
+//           and only when it survives the prune test (search_core.hpp:166)
+//           materialise it with filter_classes (label_classes.cpp:80-108)
+//           and descend
+//   cont    then the "v unmatched" continuation at the same level, itself a
+//           counted node (search_core.hpp:201-212)
+//   pop     back to the parent level
 //
-// Per u candidate the child's bound is computed first from the parent's
-// register-resident classes (one popcount pass + one warp reduction); the
-// child is only materialised (split + compaction into the next stack level)
-// when it survives the prune test. The child is still a counted node either
-// way, in the reference's order, so with donation off ("parity mode") the
-// kernel reproduces solve()'s node count and mapping exactly.
-#include <cuda_runtime.h>
-
-#include <cstdint>
-
-#include "mcsg_device.h"
+// Two specialisations:
+//   PAR = true   parity mode: one warp per instance, no donation; the host
+//                keeps the reference's vertex ids so the DFS visits the
+//                reference's nodes in the reference's order (tests compare
+//                node counts and mappings exactly).
+//   PAR = false  throughput mode: every resident warp, subtree donation to
+//                idle warps, group incumbent shared through HBM. The host
+//                relabels G in (degree desc, id asc) order so select_vertex
+//                is a single ctz; class ties break on that order.
+#include "mcsg_search.cuh"
 
 namespace mcsg {
 
-constexpr unsigned kFull = 0xffffffffu;
-constexpr unsigned kNoKey = 0xffffffffu;
-
-template <typename W>
-struct Cls {
-    W l, r;
-};
-
-template <typename W>
-struct Bits;
-template <>
-struct Bits<uint32_t> {
-    static constexpr int n = 32;
-    static constexpr int slots = 1;
-    __device__ static __forceinline__ int popc(uint32_t x) { return __popc(x); }
-    __device__ static __forceinline__ int ctz(uint32_t x) { return __ffs(x) - 1; }
-};
-template <>
-struct Bits<uint64_t> {
-    static constexpr int n = 64;
-    static constexpr int slots = 2;
-    __device__ static __forceinline__ int popc(uint64_t x) { return __popcll(x); }
-    __device__ static __forceinline__ int ctz(uint64_t x) { return __ffsll(x) - 1; }
-};
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ int ld_volatile(const int32_t* p) {
-    return *reinterpret_cast<const volatile int32_t*>(p);
-}
-__device__ __forceinline__ unsigned ld_volatile_u(const uint32_t* p) {
-    return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-
-// select_label_class key (label_classes.cpp:47-67): min over classes of
-// (max(|L|,|R|), min(|L|,|R|), lowest left id); low 7 bits carry the slot.
-template <typename W>
-__device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
-    const unsigned mx = max(pl, pr), mn = min(pl, pr);
-    return (mx << 20) | (mn << 13) | (unsigned(Bits<W>::ctz(l)) << 7) | unsigned(slot);
-}
-
-// Packed DFS frame (one per search level): where the level's classes are,
-// which class/vertex it branches on, its bound, whether the v-unmatched
-// continuation is still owned, and the u of the child being explored.
-__device__ __forceinline__ unsigned long long pack_frame(int base, int nc, int sel, int v, int bound,
-                                                         int cont, int u) {
-    return (unsigned long long)base | ((unsigned long long)nc << 14) |
-           ((unsigned long long)sel << 21) | ((unsigned long long)v << 28) |
-           ((unsigned long long)bound << 34) | ((unsigned long long)cont << 41) |
-           ((unsigned long long)u << 42);
-}
-__device__ __forceinline__ int fr_base(unsigned long long f) { return int(f & 0x3fff); }
-__device__ __forceinline__ int fr_nc(unsigned long long f) { return int((f >> 14) & 0x7f); }
-__device__ __forceinline__ int fr_sel(unsigned long long f) { return int((f >> 21) & 0x7f); }
-__device__ __forceinline__ int fr_v(unsigned long long f) { return int((f >> 28) & 0x3f); }
-__device__ __forceinline__ int fr_bound(unsigned long long f) { return int((f >> 34) & 0x7f); }
-__device__ __forceinline__ int fr_cont(unsigned long long f) { return int((f >> 41) & 1); }
-__device__ __forceinline__ int fr_u(unsigned long long f) { return int((f >> 42) & 0x3f); }
-
-// Per-warp shared-memory image; the class stack follows it.
-template <typename W, bool DIR>
-struct WarpSmem {
-    static constexpr int NB = Bits<W>::n;
-    W out_g[NB];
-    W out_h[NB];
-    W in_g[DIR ? NB : 1];
-    W in_h[DIR ? NB : 1];
-    unsigned long long f_word[kMaxDepth + 1];
-    W f_cand[kMaxDepth + 1];
-    uint16_t vkey[NB];
-    uint8_t map_v[kMaxDepth + 1];  // mapping prefix below the task's root level
-    uint8_t map_u[kMaxDepth + 1];
-};
-
-template <typename W, bool DIR>
-__host__ __device__ constexpr int warp_smem_fixed() {
-    return (int)((sizeof(WarpSmem<W, DIR>) + 15) & ~size_t(15));
-}
-
-template <typename W, bool DIR>
-__host__ __device__ constexpr int warp_smem_bytes(int classes) {
-    return (warp_smem_fixed<W, DIR>() + classes * int(sizeof(Cls<W>)) + 15) & ~15;
-}
-
-// The per-warp search state held in registers plus its views of memory.
-template <typename W, bool DIR>
-struct Search {
-    static constexpr int S = Bits<W>::slots;
-    static constexpr int NB = Bits<W>::n;
-    static constexpr int P = DIR ? 4 : 2;  // split parts (codes 0..3 / 0..1)
-
-    WarpSmem<W, DIR>& s;
-    Cls<W>* scls;   // shared-memory class stack
-    Cls<W>* gcls;   // HBM spill area (64-bit kernel)
-    int cap;
-    int lane;
-    unsigned lt;
-
-    // class (lane + 32*k) of the current level
-    W L[S], R[S];
-    W LX[S];        // L with the branching vertex v removed
-    int lc[S][P];   // |LX ∩ part_q(v)|
-
-    __device__ __forceinline__ Cls<W>* at(int base) const {
-        return base < cap ? scls + base : gcls + (base - cap);
-    }
-
-    __device__ __forceinline__ void load_level(int base, int nc) {
-        const Cls<W>* p = at(base);
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const int c = lane + 32 * k;
-            Cls<W> x{0, 0};
-            if (c < nc) x = p[c];
-            L[k] = x.l;
-            R[k] = x.r;
-        }
-    }
-
-    // compute_bound + select_label_class over the register-resident level
-    __device__ __forceinline__ unsigned scan_key(int nc, unsigned* sum) const {
-        unsigned key = kNoKey, sm = 0;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const int c = lane + 32 * k;
-            if (c < nc) {
-                const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
-                sm += unsigned(min(pl, pr));
-                key = min(key, class_key<W>(pl, pr, L[k], c));
-            }
-        }
-        if (sum) *sum = __reduce_add_sync(kFull, sm);
-        return __reduce_min_sync(kFull, key);
-    }
-
-    // select_vertex (label_classes.cpp:69-78): max degree, lowest id on ties
-    __device__ __forceinline__ int select_vertex(W lsel) const {
-        unsigned k = kNoKey;
-#pragma unroll
-        for (int b = 0; b < S; ++b) {
-            const int xb = lane + 32 * b;
-            if ((lsel >> xb) & 1) k = min(k, unsigned(s.vkey[xb]));
-        }
-        return int(__reduce_min_sync(kFull, k) & 63u);
-    }
-
-    __device__ __forceinline__ W class_l(int c) const {
-        if constexpr (S == 1) {
-            return __shfl_sync(kFull, L[0], c);
-        } else {
-            const W a = __shfl_sync(kFull, L[0], c & 31), b = __shfl_sync(kFull, L[1], c & 31);
-            return c < 32 ? a : b;
-        }
-    }
-    __device__ __forceinline__ W class_r(int c) const {
-        if constexpr (S == 1) {
-            return __shfl_sync(kFull, R[0], c);
-        } else {
-            const W a = __shfl_sync(kFull, R[0], c & 31), b = __shfl_sync(kFull, R[1], c & 31);
-            return c < 32 ? a : b;
-        }
-    }
-
-    __device__ __forceinline__ void g_parts(int v, W g[P]) const {
-        const W ao = s.out_g[v];
-        if constexpr (!DIR) {
-            g[0] = ~ao;
-            g[1] = ao;
-        } else {
-            const W ai = s.in_g[v];
-            g[0] = ~(ao | ai);
-            g[1] = ao & ~ai;
-            g[2] = ai & ~ao;
-            g[3] = ao & ai;
-        }
-    }
-    __device__ __forceinline__ void h_parts(int u, W h[P]) const {
-        const W bo = s.out_h[u];
-        if constexpr (!DIR) {
-            h[0] = ~bo;
-            h[1] = bo;
-        } else {
-            const W bi = s.in_h[u];
-            h[0] = ~(bo | bi);
-            h[1] = bo & ~bi;
-            h[2] = bi & ~bo;
-            h[3] = bo & bi;
-        }
-    }
-
-    // After choosing v: LX = L \ {v}, and the per-part left counts.
-    __device__ __forceinline__ void prep_v(int v) {
-        W g[P];
-        g_parts(v, g);
-        const W vb = W(1) << v;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            LX[k] = L[k] & ~vb;
-            if constexpr (!DIR) {
-                const int a = Bits<W>::popc(LX[k] & g[1]);
-                lc[k][1] = a;
-                lc[k][0] = Bits<W>::popc(LX[k]) - a;
-            } else {
-#pragma unroll
-                for (int q = 0; q < P; ++q) lc[k][q] = Bits<W>::popc(LX[k] & g[q]);
-            }
-        }
-    }
-
-    // Bound of the child (v,u) minus |M|+1: Σ_c Σ_parts min(|L_part|, |R_part|).
-    __device__ __forceinline__ unsigned child_sum(int u, const W h[P]) const {
-        const W ub = W(1) << u;
-        unsigned sm = 0;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const W rx = R[k] & ~ub;
-            if constexpr (!DIR) {
-                const int b = Bits<W>::popc(rx & h[1]);
-                const int r0 = Bits<W>::popc(rx) - b;
-                sm += unsigned(min(lc[k][0], r0) + min(lc[k][1], b));
-            } else {
-#pragma unroll
-                for (int q = 0; q < P; ++q) sm += unsigned(min(lc[k][q], Bits<W>::popc(rx & h[q])));
-            }
-        }
-        return __reduce_add_sync(kFull, sm);
-    }
-
-    // filter_classes (label_classes.cpp:80-108): split every class by the
-    // codes toward (v,u), drop one-sided parts, compact into the next level
-    // with ballots; returns the child's class count and its best class key.
-    __device__ __forceinline__ int split(int u, int v, const W h[P], int cbase, unsigned* key_out) {
-        W g[P];
-        g_parts(v, g);
-        const W ub = W(1) << u;
-        Cls<W>* q = at(cbase);
-        int total = 0;
-        unsigned key = kNoKey;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const W rx = R[k] & ~ub;
-#pragma unroll
-            for (int pp = 0; pp < P; ++pp) {
-                const W lp = LX[k] & g[pp], rp = rx & h[pp];
-                const bool keep = (lp != 0) & (rp != 0);
-                const unsigned m = __ballot_sync(kFull, keep);
-                if (keep) {
-                    const int pos = total + __popc(m & lt);
-                    q[pos] = Cls<W>{lp, rp};
-                    key = min(key, class_key<W>(lc[k][pp], Bits<W>::popc(rp), lp, pos));
-                }
-                total += __popc(m);
-            }
-        }
-        *key_out = __reduce_min_sync(kFull, key);
-        return total;
-    }
-};
-
-template <typename W, bool DIR>
+template <typename W, bool DIR, bool PAR>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
     mcs_search_kernel(KernelParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using Sm = WarpSmem<W, DIR>;
     using X = Search<W, DIR>;
     constexpr int NB = Bits<W>::n;
-    constexpr int S = Bits<W>::slots;
     constexpr int P = X::P;
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
+    // warp index via a warp reduction: the result lives in a uniform register,
+    // so the per-warp shared-memory addresses below stay in the uniform
+    // datapath instead of being rematerialised from SR_TID in the hot loop
+    const int wib = int(__reduce_min_sync(kFull, threadIdx.x >> 5));
     const int gw = blockIdx.x * kWarpsPerCta + wib;
     const int per_warp = warp_smem_bytes<W, DIR>(p.smem_classes);
     Sm& s = *reinterpret_cast<Sm*>(smem_raw + size_t(wib) * per_warp);
@@ -344,13 +57,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         {}};
     const int stack_limit = p.smem_classes + p.spill_classes;
     Ctl* const ctl = p.ctl;
+    const int interval = p.poll_interval;
 
     const unsigned long long t_warp0 = globaltimer();
     const unsigned long long deadline = p.budget_ns ? t_warp0 + p.budget_ns : 0ull;
     if (lane == 0) atomicMin(&p.counters->t_start_ns, t_warp0);
 
-    unsigned long long nodes = 0, sum_cls = 0, splits = 0, split_cls = 0, donations = 0;
-    unsigned long long tasks = 0, spills = 0;
+    if (lane == 0) s.st_nodes = s.st_splits = s.st_donations = s.st_tasks = s.st_spills = 0;
     int cur_inst = -1;
     int maxp = 0, goal = 0, prune = 1, floor_sz = 0, grp = 0;
     bool stop_all = false;
@@ -376,7 +89,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 }
                 int ok = 0;
                 unsigned long long pos = 0;
-                if (lane == 0) {
+                if (!PAR && lane == 0) {
                     // cheap emptiness test before touching the ring
                     pos = ld_relaxed(&ctl->head.v);
                     if (ld_relaxed(&ctl->tail.v) != pos) {
@@ -406,6 +119,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                     branch = true;
                     break;
                 }
+                if (PAR) break;  // parity mode: roots only
                 int pend = 0, st = 0;
                 if (lane == 0) {
                     if (!registered_idle) atomicAdd(&ctl->idle.v, 1);
@@ -441,7 +155,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                     s.in_g[i] = W(dsc.in_g[i]);
                     s.in_h[i] = W(dsc.in_h[i]);
                 }
-                s.vkey[i] = dsc.vkey[i];
+                if constexpr (PAR) s.vkey[i] = dsc.vkey[i];
             }
             maxp = dsc.maxp;
             goal = dsc.goal;
@@ -452,11 +166,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         }
         GroupState* const gs = p.grp + grp;
         InstanceState* const is = p.ist + inst;
-        ++tasks;
+        if (lane == 0) {
+            s.st_tasks += 1;
+            s.polled = 0;
+        }
 
-        // Best sizes: best_local backs offers (LocalIncumbent::offer compares
-        // with its own mapping only, search_core.hpp:29-31); best_eff adds the
-        // external floor and, when sharing, the group incumbent (size()).
+        // Incumbent sizes. Parity: offers compare with the warp's own mapping
+        // (LocalIncumbent::offer, search_core.hpp:29-31) and pruning adds the
+        // external floor (size(), :25-28). Throughput: both use the group size.
         int best_local = 0, best_eff = floor_sz;
         bool skip = false;
         {
@@ -467,16 +184,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             }
             gb = __shfl_sync(kFull, gb, 0);
             gd = __shfl_sync(kFull, gd, 0);
-            if (p.donate) best_eff = max(best_eff, gb);
+            if (!PAR) best_eff = max(best_eff, gb);
             skip = gd != 0;
         }
+        int off_thr = PAR ? best_local : best_eff;                  // offer when |M| > off_thr
+        int prn_thr = prune ? max(best_eff, goal - 1) : -1;         // prune when bound <= prn_thr
+        auto raise_best = [&](int b) {
+            best_local = max(best_local, b);
+            best_eff = max(best_eff, b);
+            off_thr = PAR ? best_local : best_eff;
+            prn_thr = prune ? max(best_eff, goal - 1) : -1;
+        };
 
         int d, root, base = 0, nc, bound, sel = 0, v = 0;
         W cand = 0;
         int cont = 0;
         unsigned key = kNoKey;
         bool have_key = false;
-        bool at_next = false;  // true: resume the u loop of the current level
+        bool at_next = false;  // true: resume the u loop of the task's level
         if (!branch) {
             const InstanceDesc& dsc = p.inst[inst];
             nc = dsc.n_init;
@@ -507,14 +232,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             x.prep_v(v);
             at_next = true;
             // task-level prune (engine_parallel.cpp:148-155): every child would prune
-            if (p.donate && prune && bound <= max(best_eff, goal - 1)) skip = true;
+            if (bound <= prn_thr) skip = true;
         }
 
-        unsigned long long task_nodes = 0, next_poll = p.poll_interval;
+        int cd = interval;     // nodes until the next poll
+        unsigned splits = 0;   // flushed to s.st_splits at polls and at the task's end
         bool abort_all = false;
 
-        // Writes M ∪ {(v,u)} (|M| = dd) as the instance's mapping if it is
-        // still an improvement there; raises the group size afterwards.
+        // Stores M ∪ {(v,u)} (|M| = dd) as the instance's mapping if it still
+        // improves there, then raises the group size (an incumbent size never
+        // exceeds a mapping actually written).
         auto offer = [&](int dd, int uu) {
             int stored = 0;
             if (lane == 0)
@@ -571,21 +298,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                     atomicCAS(&ctl->stop.v, 0, 2);
                     st = 2;
                 }
-                gb = int(ld_volatile_u(&gs->best));
-                gd = int(ld_volatile_u(&gs->done));
-                if (p.donate) idl = ld_volatile(&ctl->idle.v);
+                if (!PAR) {
+                    gb = int(ld_volatile_u(&gs->best));
+                    gd = int(ld_volatile_u(&gs->done));
+                    idl = ld_volatile(&ctl->idle.v);
+                }
             }
             st = __shfl_sync(kFull, st, 0);
-            gd = __shfl_sync(kFull, gd, 0);
             if (st != 0) {
                 abort_all = true;
                 return false;
             }
+            if (PAR) return true;
+            gd = __shfl_sync(kFull, gd, 0);
             if (gd != 0) return false;
-            if (!p.donate) return true;
             gb = __shfl_sync(kFull, gb, 0);
             idl = __shfl_sync(kFull, idl, 0);
-            best_eff = max(best_eff, gb);
+            if (gb > best_eff) raise_best(gb);
             if (idl <= 0 || d <= root) return true;
             // donate the shallowest level that still owns work
             int f = -1;
@@ -669,17 +398,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             }
             __threadfence();
             __syncwarp();
-            if (lane == 0) st_release(&sl->seq, pos + 1);
-            ++donations;
+            if (lane == 0) {
+                st_release(&sl->seq, pos + 1);
+                s.st_donations += 1;
+            }
             return true;
         };
+
+// one counted search node (search_core.hpp:130), with the periodic poll
+#define MCSG_COUNT_NODE()                       \
+    if (--cd == 0) {                            \
+        if (lane == 0) {                        \
+            s.polled += unsigned(interval);     \
+            s.st_splits += splits;              \
+        }                                       \
+        splits = 0;                             \
+        cd = interval;                          \
+        if (!poll()) goto finish;               \
+    }
 
         if (!skip) {
             if (!at_next) {
                 // the root node (search_core.hpp:129-166)
-                ++task_nodes;
-                sum_cls += unsigned(nc);
-                if (prune && bound <= max(best_eff, goal - 1)) goto pop;
+                MCSG_COUNT_NODE();
+                if (bound <= prn_thr) goto pop;
                 goto select;
             }
             goto next;
@@ -691,7 +433,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             sel = int(key & 127u);
             {
                 const W lsel = x.class_l(sel);
-                v = x.select_vertex(lsel);
+                if constexpr (PAR) v = x.select_vertex(lsel);
+                else v = Bits<W>::ctz(lsel);  // G is relabelled in select_vertex order
                 cand = x.class_r(sel);
             }
             x.prep_v(v);
@@ -702,11 +445,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             while (cand != 0) {
                 const int u = Bits<W>::ctz(cand);
                 cand &= cand - 1;
-                ++task_nodes;  // the child's entry (search_core.hpp:130)
-                if (d + 1 > (p.donate ? best_eff : best_local)) {
+                MCSG_COUNT_NODE();  // the child's entry
+                if (d + 1 > off_thr) {
                     offer(d, u);
-                    best_local = d + 1;
-                    best_eff = max(best_eff, d + 1);
+                    raise_best(d + 1);
                     if (goal > 0 && d + 1 >= goal) {  // search_core.hpp:147-150
                         if (lane == 0) {
                             gs->reached = 1;
@@ -719,20 +461,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                         goto finish;
                     }
                 }
-                if (task_nodes >= next_poll) {
-                    next_poll = task_nodes + p.poll_interval;
-                    if (!poll()) goto finish;
-                }
                 W h[P];
                 x.h_parts(u, h);
                 const int cbound = d + 1 + int(x.child_sum(u, h));
-                if (prune && cbound <= max(best_eff, goal - 1)) continue;  // pruned child
+                if (cbound <= prn_thr) continue;  // pruned at entry
                 // ---- materialise the child (filter_classes) one level up
                 int cb = base + nc;
                 const int need = min(nc * P, NB);
                 if (cb < x.cap && cb + need > x.cap) {
                     cb = x.cap;
-                    ++spills;
+                    if (lane == 0) s.st_spills += 1;
                 }
                 if (cb + need > stack_limit) {  // cannot happen with the host's sizing
                     if (lane == 0) {
@@ -750,12 +488,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 const int cnc = x.split(u, v, h, cb, &ckey);
                 __syncwarp();
                 ++splits;
-                split_cls += unsigned(nc);
                 ++d;
                 base = cb;
                 nc = cnc;
                 bound = cbound;
-                sum_cls += unsigned(nc);
                 x.load_level(base, nc);
                 key = ckey;
                 have_key = true;
@@ -763,25 +499,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             }
             // ---- v left unmatched (search_core.hpp:201-212): a counted node
             if (cont) {
-                ++task_nodes;
-                if (task_nodes >= next_poll) {
-                    next_poll = task_nodes + p.poll_interval;
-                    if (!poll()) goto finish;
-                }
+                MCSG_COUNT_NODE();
                 const W lsel = x.class_l(sel), rsel = x.class_r(sel);
                 bound -= (Bits<W>::popc(lsel) <= Bits<W>::popc(rsel)) ? 1 : 0;
                 const W nl = lsel & ~(W(1) << v);
                 Cls<W>* lvl = x.at(base);
                 if (nl != 0) {
 #pragma unroll
-                    for (int k = 0; k < S; ++k)
+                    for (int k = 0; k < X::S; ++k)
                         if (lane + 32 * k == sel) x.L[k] = nl;
                     if (lane == 0) lvl[sel].l = nl;
                 } else {
                     // drop the emptied class: the last class takes its slot
                     const W ll = x.class_l(nc - 1), lr = x.class_r(nc - 1);
 #pragma unroll
-                    for (int k = 0; k < S; ++k) {
+                    for (int k = 0; k < X::S; ++k) {
                         const int c = lane + 32 * k;
                         if (c == nc - 1) {  // lanes past the level must hold empty classes
                             x.L[k] = 0;
@@ -797,9 +529,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 }
                 __syncwarp();
                 cont = 0;
-                sum_cls += unsigned(nc);
                 have_key = false;
-                if (prune && bound <= max(best_eff, goal - 1)) goto pop;
+                if (bound <= prn_thr) goto pop;
                 goto select;
             }
 
@@ -821,9 +552,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             x.prep_v(v);
             goto next;
         }
-    finish:
-        nodes += task_nodes;
+#undef MCSG_COUNT_NODE
+    finish : {
         if (lane == 0) {
+            const unsigned long long task_nodes = s.polled + unsigned(interval - cd);
+            s.st_nodes += task_nodes;
+            s.st_splits += splits;
             if (task_nodes) atomicAdd(&is->nodes, task_nodes);
             if (!abort_all) {
                 const int left = atomicSub(&is->open_tasks, 1) - 1;
@@ -835,45 +569,47 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 atomicSub(&ctl->pending.v, 1);
             }
         }
+    }
         if (abort_all) stop_all = true;
         __syncwarp();
     }
 
     if (lane == 0) {
         Counters* c = p.counters;
-        atomicAdd(&c->nodes, nodes);
-        atomicAdd(&c->sum_classes, sum_cls);
-        atomicAdd(&c->splits, splits);
-        atomicAdd(&c->split_classes, split_cls);
-        atomicAdd(&c->donations, donations);
-        atomicAdd(&c->tasks, tasks);
-        atomicAdd(&c->spills, spills);
+        atomicAdd(&c->nodes, s.st_nodes);
+        atomicAdd(&c->splits, s.st_splits);
+        atomicAdd(&c->donations, s.st_donations);
+        atomicAdd(&c->tasks, s.st_tasks);
+        atomicAdd(&c->spills, s.st_spills);
     }
-    (void)S;
 }
 
 // ------------------------------------------------------------ host launch --
-template <typename W, bool DIR>
+template <typename W, bool DIR, bool PAR>
 static cudaError_t launch_t(const KernelParams& p, int ctas, cudaStream_t st) {
     const int smem = warp_smem_bytes<W, DIR>(p.smem_classes) * kWarpsPerCta;
-    cudaError_t e = cudaFuncSetAttribute(mcs_search_kernel<W, DIR>,
+    cudaError_t e = cudaFuncSetAttribute(mcs_search_kernel<W, DIR, PAR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    mcs_search_kernel<W, DIR><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
+    mcs_search_kernel<W, DIR, PAR><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <typename W, bool DIR>
 static int occupancy_t(int smem_classes) {
     const int smem = warp_smem_bytes<W, DIR>(smem_classes) * kWarpsPerCta;
-    if (cudaFuncSetAttribute(mcs_search_kernel<W, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess)
-        return 0;
-    int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, mcs_search_kernel<W, DIR>,
-                                                      kWarpsPerCta * 32, smem) != cudaSuccess)
-        return 0;
-    return blocks;
+    int worst = 1 << 30;
+    for (int par = 0; par < 2; ++par) {
+        auto fn = par ? mcs_search_kernel<W, DIR, true> : mcs_search_kernel<W, DIR, false>;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return 0;
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kWarpsPerCta * 32, smem) !=
+            cudaSuccess)
+            return 0;
+        worst = blocks < worst ? blocks : worst;
+    }
+    return worst;
 }
 
 int kernel_smem_per_warp(bool wide, bool directed, int smem_classes) {
@@ -890,11 +626,18 @@ int kernel_occupancy(bool wide, bool directed, int smem_classes) {
                     : occupancy_t<uint32_t, false>(smem_classes);
 }
 
-cudaError_t kernel_launch(bool wide, bool directed, const KernelParams& p, int ctas,
+cudaError_t kernel_launch(bool wide, bool directed, bool parity, const KernelParams& p, int ctas,
                           cudaStream_t st) {
-    if (wide) return directed ? launch_t<uint64_t, true>(p, ctas, st)
-                              : launch_t<uint64_t, false>(p, ctas, st);
-    return directed ? launch_t<uint32_t, true>(p, ctas, st) : launch_t<uint32_t, false>(p, ctas, st);
+    if (parity) {
+        if (wide) return directed ? launch_t<uint64_t, true, true>(p, ctas, st)
+                                  : launch_t<uint64_t, false, true>(p, ctas, st);
+        return directed ? launch_t<uint32_t, true, true>(p, ctas, st)
+                        : launch_t<uint32_t, false, true>(p, ctas, st);
+    }
+    if (wide) return directed ? launch_t<uint64_t, true, false>(p, ctas, st)
+                              : launch_t<uint64_t, false, false>(p, ctas, st);
+    return directed ? launch_t<uint32_t, true, false>(p, ctas, st)
+                    : launch_t<uint32_t, false, false>(p, ctas, st);
 }
 
 // Resets the ring (slot i of lap 0 expects producer ticket i) and the
