@@ -104,6 +104,8 @@ typedef struct mcsg_stats {
     uint64_t h2d_bytes;      /* bytes copied host->device by the call */
     uint64_t d2h_bytes;      /* bytes copied device->host by the call */
     uint64_t launches;       /* kernels launched by the call */
+    uint64_t busy_cycles;    /* Σ over warps of SM cycles running tasks */
+    uint64_t idle_cycles;    /* Σ over warps of SM cycles waiting for a task */
 } mcsg_stats;
 
 typedef struct mcsg_result {

@@ -104,7 +104,8 @@ class _Stats(C.Structure):
                 ("spills", C.c_uint64), ("probes", C.c_uint64), ("wall_s", C.c_double),
                 ("kernel_s", C.c_double), ("h2d_s", C.c_double), ("warps", C.c_int32),
                 ("ctas", C.c_int32), ("smem_per_cta", C.c_int32), ("smem_classes", C.c_int32),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64),
+                ("busy_cycles", C.c_uint64), ("idle_cycles", C.c_uint64)]
 
 
 class _Result(C.Structure):
@@ -393,6 +394,8 @@ class SearchStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     launches: int = 0
+    busy_cycles: int = 0
+    idle_cycles: int = 0
 
 
 @dataclass
@@ -440,6 +443,7 @@ def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
         s.donations, s.tasks, s.spills = int(st.donations), int(st.tasks), int(st.spills)
         s.warps, s.ctas, s.smem_per_cta, s.smem_classes = st.warps, st.ctas, st.smem_per_cta, st.smem_classes
         s.h2d_bytes, s.d2h_bytes, s.launches = int(st.h2d_bytes), int(st.d2h_bytes), int(st.launches)
+        s.busy_cycles, s.idle_cycles = int(st.busy_cycles), int(st.idle_cycles)
     return SolveResult(SolveStatus(r.status), pairs, int(r.size), s)
 
 

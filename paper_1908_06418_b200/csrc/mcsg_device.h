@@ -101,6 +101,8 @@ struct Counters {
     unsigned long long spills;       // levels placed in the HBM spill area
     unsigned long long t_start_ns;   // min %globaltimer over warps at kernel start
     unsigned long long overflow;     // class-stack overflow (must stay 0)
+    unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
+    unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks
 };
 
 // Control words of one launch, one 128-byte line each so that idle warps

@@ -259,6 +259,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
             smem_classes -= 16;
     }
     smem_classes = std::max(smem_classes, 64);
+    if (!wide) smem_classes = std::max(smem_classes, path_bound);  // 32-bit kernel: no spill path
     blocks = kernel_occupancy(wide, directed, smem_classes);
     if (blocks <= 0) throw Error("requested shared-memory class stack does not fit");
     int ctas = blocks * ctx.sms;
@@ -299,7 +300,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
     p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
     p.spill = ctx.d_spill;
-    p.spill_classes = kSpillClasses;
+    p.spill_classes = wide ? kSpillClasses : 0;
     p.smem_classes = smem_classes;
     p.donate = parity ? 0 : 1;
     p.poll_interval = parity ? 4096 : 256;
@@ -389,6 +390,8 @@ void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probe
     st->h2d_bytes = lo.h2d_bytes;
     st->d2h_bytes = lo.d2h_bytes;
     st->launches = lo.launches;
+    st->busy_cycles = lo.counters.busy_cycles;
+    st->idle_cycles = lo.counters.idle_cycles;
 }
 
 void accumulate(mcsg_stats* st, const LaunchOut& lo) {
@@ -409,6 +412,8 @@ void accumulate(mcsg_stats* st, const LaunchOut& lo) {
     st->h2d_bytes += lo.h2d_bytes;
     st->d2h_bytes += lo.d2h_bytes;
     st->launches += lo.launches;
+    st->busy_cycles += lo.counters.busy_cycles;
+    st->idle_cycles += lo.counters.idle_cycles;
 }
 
 mcsg_options defaults(const mcsg_options* o) {

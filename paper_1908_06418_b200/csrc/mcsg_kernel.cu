@@ -63,10 +63,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
     const unsigned long long deadline = p.budget_ns ? t_warp0 + p.budget_ns : 0ull;
     if (lane == 0) atomicMin(&p.counters->t_start_ns, t_warp0);
 
-    if (lane == 0) s.st_nodes = s.st_splits = s.st_donations = s.st_tasks = s.st_spills = 0;
+    if (lane == 0) s.st_nodes = s.st_splits = s.st_donations = s.st_tasks = s.st_spills = s.st_idle = s.st_busy = 0;
+    long long t_mark = clock64();
     int cur_inst = -1;
     int maxp = 0, goal = 0, prune = 1, floor_sz = 0, grp = 0;
     bool stop_all = false;
+    bool have_ticket = false;
+    unsigned long long ticket = 0;
 
     while (!stop_all) {
         // ---------------------------------------------------------- acquire
@@ -74,66 +77,64 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         bool branch = false;
         unsigned long long slot_pos = 0;
         {
+            // Roots first (an atomic counter over instance ids), then the
+            // ticket ring: a warp out of roots takes ONE ticket with atomicAdd
+            // on head and waits on its own slot until the producer holding
+            // the same ticket publishes it. No CAS retries on a shared word;
+            // head - tail is the number of waiting warps (the donation
+            // trigger). A waiting warp leaves when pending drops to 0: then
+            // no task is queued or running, so no producer can follow.
             bool got = false;
-            bool registered_idle = false;
             unsigned backoff = 64;
+            int spins = 0;
             for (;;) {
-                int r = p.n_inst;
-                if (lane == 0 && ld_volatile(&ctl->next_root.v) < p.n_inst)
-                    r = atomicAdd(&ctl->next_root.v, 1);
-                r = __shfl_sync(kFull, r, 0);
-                if (r < p.n_inst) {
-                    inst = r;
-                    got = true;
-                    break;
+                if (!have_ticket) {
+                    int r = p.n_inst;
+                    if (lane == 0 && ld_volatile(&ctl->next_root.v) < p.n_inst)
+                        r = atomicAdd(&ctl->next_root.v, 1);
+                    r = __shfl_sync(kFull, r, 0);
+                    if (r < p.n_inst) {
+                        inst = r;
+                        got = true;
+                        break;
+                    }
+                    if (PAR) break;  // parity mode: roots only
+                    unsigned long long t = 0;
+                    if (lane == 0) t = atomicAdd(&ctl->head.v, 1ull);
+                    ticket = __shfl_sync(kFull, t, 0);
+                    have_ticket = true;
                 }
                 int ok = 0;
-                unsigned long long pos = 0;
-                if (!PAR && lane == 0) {
-                    // cheap emptiness test before touching the ring
-                    pos = ld_relaxed(&ctl->head.v);
-                    if (ld_relaxed(&ctl->tail.v) != pos) {
-                        for (int tries = 0; tries < 8; ++tries) {
-                            TaskSlot* sl = p.slots + (pos & p.cap_mask);
-                            const unsigned long long seq = ld_acquire(&sl->seq);
-                            const long long dif = (long long)(seq - (pos + 1));
-                            if (dif == 0) {
-                                const unsigned long long prev = atomicCAS(&ctl->head.v, pos, pos + 1);
-                                if (prev == pos) {
-                                    ok = 1;
-                                    break;
-                                }
-                                pos = prev;
-                            } else if (dif < 0) {
-                                break;  // not yet published / empty
-                            } else {
-                                pos = ld_relaxed(&ctl->head.v);
-                            }
-                        }
-                    }
+                if (lane == 0) {
+                    const TaskSlot* sl = p.slots + (ticket & p.cap_mask);
+                    ok = ld_acquire(&sl->seq) == ticket + 1;
                 }
                 ok = __shfl_sync(kFull, ok, 0);
                 if (ok) {
-                    slot_pos = __shfl_sync(kFull, pos, 0);
+                    slot_pos = ticket;
+                    have_ticket = false;
                     got = true;
                     branch = true;
                     break;
                 }
-                if (PAR) break;  // parity mode: roots only
-                int pend = 0, st = 0;
-                if (lane == 0) {
-                    if (!registered_idle) atomicAdd(&ctl->idle.v, 1);
-                    pend = ld_volatile(&ctl->pending.v);
-                    st = ld_volatile(&ctl->stop.v);
+                if ((++spins & 7) == 0) {
+                    int pend = 0, st = 0;
+                    if (lane == 0) {
+                        pend = ld_volatile(&ctl->pending.v);
+                        st = ld_volatile(&ctl->stop.v);
+                    }
+                    pend = __shfl_sync(kFull, pend, 0);
+                    st = __shfl_sync(kFull, st, 0);
+                    if (pend <= 0 || st != 0) break;
                 }
-                registered_idle = true;
-                pend = __shfl_sync(kFull, pend, 0);
-                st = __shfl_sync(kFull, st, 0);
-                if (pend <= 0 || st != 0) break;
-                __nanosleep(backoff + (gw & 63) * 8);
-                if (backoff < 4096) backoff <<= 1;
+                __nanosleep(backoff + (gw & 31) * 8);
+                if (backoff < 1024) backoff <<= 1;
             }
-            if (registered_idle && lane == 0) atomicSub(&ctl->idle.v, 1);
+            {
+                const long long t = clock64();
+                if (lane == 0) s.st_idle += (unsigned long long)(t - t_mark);
+                t_mark = t;
+            }
             if (!got) break;
         }
 
@@ -187,6 +188,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             if (!PAR) best_eff = max(best_eff, gb);
             skip = gd != 0;
         }
+        // prefetch the control words the first poll will read
+        auto prefetch_ctl = [&]() {
+            if (lane == 0) cp_async16(&s.pf[0], &ctl->stop);
+            if (!PAR && lane == 1) cp_async16(&s.pf[4], &ctl->head);
+            if (!PAR && lane == 2) cp_async16(&s.pf[8], &ctl->tail);
+            if (!PAR && lane == 3) cp_async16(&s.pf[12], gs);
+            cp_async_commit();
+        };
+        cp_async_wait_all();  // the previous task's copies must not land after these
+        __syncwarp();
+        prefetch_ctl();
         int off_thr = PAR ? best_local : best_eff;                  // offer when |M| > off_thr
         int prn_thr = prune ? max(best_eff, goal - 1) : -1;         // prune when bound <= prn_thr
         auto raise_best = [&](int b) {
@@ -287,21 +299,29 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         // Periodic poll: stop/deadline/cancel, group done, shared incumbent,
         // and subtree donation to idle warps. Returns false to end the task.
         auto poll = [&]() -> bool {
-            int st = 0, gb = 0, gd = 0, idl = 0;
-            if (lane == 0) {
-                st = ld_volatile(&ctl->stop.v);
-                if (st == 0 && deadline && globaltimer() >= deadline) {
+            // values prefetched at the previous poll (one interval stale: stale
+            // reads only delay a stop or weaken pruning)
+            cp_async_wait_all();
+            __syncwarp();
+            int st = int(s.pf[0]);
+            long long waiting = 0;  // warps holding a ticket no producer has served yet
+            if (!PAR) {
+                const unsigned long long hd = (unsigned long long)s.pf[4] | ((unsigned long long)s.pf[5] << 32);
+                const unsigned long long tl = (unsigned long long)s.pf[8] | ((unsigned long long)s.pf[9] << 32);
+                waiting = (long long)(hd - tl);
+            }
+            const int gb = PAR ? 0 : int(s.pf[12]);  // GroupState::best
+            const int gd = PAR ? 0 : int(s.pf[13]);  // GroupState::done
+            __syncwarp();
+            prefetch_ctl();
+            if (lane == 0 && st == 0) {
+                if (deadline && globaltimer() >= deadline) {
                     atomicCAS(&ctl->stop.v, 0, 1);
                     st = 1;
                 }
                 if (st == 0 && gw == 0 && p.cancel && *p.cancel) {
                     atomicCAS(&ctl->stop.v, 0, 2);
                     st = 2;
-                }
-                if (!PAR) {
-                    gb = int(ld_volatile_u(&gs->best));
-                    gd = int(ld_volatile_u(&gs->done));
-                    idl = ld_volatile(&ctl->idle.v);
                 }
             }
             st = __shfl_sync(kFull, st, 0);
@@ -310,12 +330,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 return false;
             }
             if (PAR) return true;
-            gd = __shfl_sync(kFull, gd, 0);
             if (gd != 0) return false;
-            gb = __shfl_sync(kFull, gb, 0);
-            idl = __shfl_sync(kFull, idl, 0);
             if (gb > best_eff) raise_best(gb);
-            if (idl <= 0 || d <= root) return true;
+            if (waiting <= 0 || d <= root) return true;
             // donate the shallowest level that still owns work
             int f = -1;
             for (int b0 = root; b0 < d && f < 0; b0 += 32) {
@@ -333,30 +350,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
             if (cnt >= 2)
                 for (int i = 0; i < (cnt + 1) / 2; ++i) give &= give - 1;  // upper half
             const W keep = fc & ~give;
-            int ok = 0;
+            // producer ticket; a warp is (probably) already waiting on it.
+            // The slot is free once the consumer of ticket pos - cap released
+            // it; the ring is far larger than the warp count, so this wait is
+            // normally zero.
             unsigned long long pos = 0;
             if (lane == 0) {
-                for (int tries = 0; tries < 16; ++tries) {
-                    pos = ld_relaxed(&ctl->tail.v);
-                    TaskSlot* sl = p.slots + (pos & p.cap_mask);
-                    const unsigned long long seq = ld_acquire(&sl->seq);
-                    const long long dif = (long long)(seq - pos);
-                    if (dif == 0) {
-                        if (atomicCAS(&ctl->tail.v, pos, pos + 1) == pos) {
-                            ok = 1;
-                            break;
-                        }
-                    } else if (dif < 0) {
-                        break;  // full
-                    }
-                }
-                if (ok) {
-                    atomicAdd(&ctl->pending.v, 1);
-                    atomicAdd(&is->open_tasks, 1);
-                }
+                atomicAdd(&ctl->pending.v, 1);
+                atomicAdd(&is->open_tasks, 1);
+                pos = atomicAdd(&ctl->tail.v, 1ull);
+                const TaskSlot* sl = p.slots + (pos & p.cap_mask);
+                while (ld_acquire(&sl->seq) != pos) __nanosleep(32);
             }
-            ok = __shfl_sync(kFull, ok, 0);
-            if (!ok) return true;
             pos = __shfl_sync(kFull, pos, 0);
             TaskSlot* sl = p.slots + (pos & p.cap_mask);
             const int fnc = fr_nc(fw);
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                 s.f_cand[f] = keep;
                 s.f_word[f] = fw & ~(1ull << 41);  // the continuation left with the task
             }
-            __threadfence();
+            fence_acq_rel_gpu();  // payload before the release of the slot
             __syncwarp();
             if (lane == 0) {
                 st_release(&sl->seq, pos + 1);
@@ -554,6 +559,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         }
 #undef MCSG_COUNT_NODE
     finish : {
+        {
+            const long long t = clock64();
+            if (lane == 0) s.st_busy += (unsigned long long)(t - t_mark);
+            t_mark = t;
+        }
         if (lane == 0) {
             const unsigned long long task_nodes = s.polled + unsigned(interval - cd);
             s.st_nodes += task_nodes;
@@ -565,7 +575,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
                     is->t_done_ns = globaltimer();
                     if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
                 }
-                __threadfence();
                 atomicSub(&ctl->pending.v, 1);
             }
         }
@@ -581,6 +590,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
         atomicAdd(&c->donations, s.st_donations);
         atomicAdd(&c->tasks, s.st_tasks);
         atomicAdd(&c->spills, s.st_spills);
+        atomicAdd(&c->idle_cycles, s.st_idle);
+        atomicAdd(&c->busy_cycles, s.st_busy);
     }
 }
 

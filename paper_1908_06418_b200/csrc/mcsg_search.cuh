@@ -86,6 +86,16 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     return v;
 }
 
+// 16-byte global -> shared copy that bypasses L1 (device-coherent values),
+// completing in the background; used to prefetch control words.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned dst = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ int ld_volatile(const int32_t* p) {
     return *reinterpret_cast<const volatile int32_t*>(p);
 }
@@ -128,9 +138,13 @@ struct WarpSmem {
     W in_g[DIR ? NB : 1];
     W in_h[DIR ? NB : 1];
     unsigned long long f_word[kMaxDepth + 1];
+    // Control words prefetched one poll ahead with cp.async (16 B each):
+    // [0..3] the stop line, [4..7] ring head, [8..11] ring tail, [12..15] GroupState.
+    alignas(16) uint32_t pf[16];
     // per-warp counters kept out of registers (written by lane 0)
     unsigned long long polled;     // nodes of the current task counted at earlier polls
     unsigned long long st_nodes, st_splits, st_donations, st_tasks, st_spills;
+    unsigned long long st_idle, st_busy;  // clock64 cycles waiting for / running tasks
     W f_cand[kMaxDepth + 1];
     uint16_t vkey[NB];
     uint8_t map_v[kMaxDepth + 1];  // mapping prefix below the task's root level
@@ -166,12 +180,21 @@ struct Search {
     W LX[S];        // L with the branching vertex v removed
     int lc[S][P];   // |LX ∩ part_q(v)|
 
+    // The 32-bit kernel never spills: the host sizes its shared stack to the
+    // path bound m(m+1)/2. The 64-bit kernel keeps levels past `cap` in HBM;
+    // a level lies entirely on one side, and the hot accessors branch on it
+    // so that the shared-memory case compiles to LDS/STS (not generic LD/ST).
+    static constexpr bool kSpill = sizeof(W) == 8;
+
+    __device__ __forceinline__ bool in_smem(int base) const { return !kSpill || base < cap; }
+
+    // generic pointer, for the rare paths (donation, continuation write-back)
     __device__ __forceinline__ Cls<W>* at(int base) const {
-        return base < cap ? scls + base : gcls + (base - cap);
+        return in_smem(base) ? scls + base : gcls + (base - cap);
     }
 
-    __device__ __forceinline__ void load_level(int base, int nc) {
-        const Cls<W>* p = at(base);
+    template <typename Ptr>
+    __device__ __forceinline__ void load_from(const Ptr* p, int nc) {
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             const int c = lane + 32 * k;
@@ -180,6 +203,11 @@ struct Search {
             L[k] = x.l;
             R[k] = x.r;
         }
+    }
+
+    __device__ __forceinline__ void load_level(int base, int nc) {
+        if (in_smem(base)) load_from(scls + base, nc);
+        else load_from(gcls + (base - cap), nc);
     }
 
     // compute_bound + select_label_class over the register-resident level
@@ -295,10 +323,14 @@ struct Search {
     // codes toward (v,u), drop one-sided parts, compact into the next level
     // with ballots; returns the child's class count and its best class key.
     __device__ __forceinline__ int split(int u, int v, const W h[P], int cbase, unsigned* key_out) {
+        if (in_smem(cbase)) return split_into(u, v, h, scls + cbase, key_out);
+        return split_into(u, v, h, gcls + (cbase - cap), key_out);
+    }
+
+    __device__ __forceinline__ int split_into(int u, int v, const W h[P], Cls<W>* q, unsigned* key_out) {
         W g[P];
         g_parts(v, g);
         const W ub = W(1) << u;
-        Cls<W>* q = at(cbase);
         int total = 0;
         unsigned key = kNoKey;
 #pragma unroll

@@ -1,0 +1,32 @@
+"""Summarise an ncu --set full report of the search kernel (dev tool)."""
+import csv, json, subprocess, sys
+rep, nodes = sys.argv[1], float(sys.argv[2])
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+r = list(csv.reader(raw))
+hdr, units, vals = r[0], r[1], r[2]
+d = dict(zip(hdr, vals)); u = dict(zip(hdr, units))
+def f(k):
+    try: return float(d[k].replace(',', ''))
+    except Exception: return None
+keys = ['gpu__time_duration.sum', 'smsp__inst_executed.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.per_cycle_active',
+        'smsp__warps_eligible.avg.per_cycle_active', 'launch__registers_per_thread',
+        'smsp__thread_inst_executed_per_inst_executed.ratio', 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum',
+        'sm__cycles_elapsed.avg']
+out = {k: f(k) for k in keys}
+out['unit'] = {k: u.get(k) for k in keys}
+pipes = {k: f(k) for k in hdr if k.startswith('sm__inst_executed_pipe_') and k.endswith('.avg.pct_of_peak_sustained_active')}
+stalls = {k.replace('smsp__pcsamp_warps_issue_stalled_', ''): f(k) for k in hdr
+          if k.startswith('smsp__pcsamp_warps_issue_stalled_') and not k.endswith('not_issued')}
+tot = sum(v for v in stalls.values() if v)
+out['warp_inst_per_node'] = out['smsp__inst_executed.sum'] / nodes
+dram = (out['dram__bytes_read.sum'] or 0) + (out['dram__bytes_write.sum'] or 0)
+if out['unit'].get('dram__bytes_read.sum') == 'Mbyte': dram *= 1e6
+elif out['unit'].get('dram__bytes_read.sum') == 'Gbyte': dram *= 1e9
+elif out['unit'].get('dram__bytes_read.sum') == 'Kbyte': dram *= 1e3
+out['dram_bytes_per_launch'] = dram
+out['nodes_per_launch'] = nodes
+out['stall_pct'] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0)) if v}
+out['pipes_pct'] = {k.replace('sm__inst_executed_pipe_', '').replace('.avg.pct_of_peak_sustained_active', ''): v
+                    for k, v in sorted(pipes.items(), key=lambda x: -(x[1] or 0)) if v}
+print(json.dumps(out, indent=1))

@@ -12,4 +12,6 @@ for i in range(n):
 res, st = M.solve_batch(pairs, M.SolveConfig(mode=mode, budget_seconds=60))
 print("nodes", st.recursions, "kernel_s", st.kernel_seconds, "rate G/s", st.recursions / st.kernel_seconds / 1e9,
       "C/node", st.sum_classes / st.recursions, "splits/node", st.splits / st.recursions,
-      "split_cls/split", st.split_classes / max(1, st.splits))
+      "split_cls/split", st.split_classes / max(1, st.splits),
+      "busy_frac", st.busy_cycles / max(1, st.busy_cycles + st.idle_cycles), "tasks", st.tasks,
+      "donations", st.donations, "busy cycles/node", st.busy_cycles / st.recursions)
