@@ -1,0 +1,158 @@
+// Drop-in adapter: the reference's C++ entry points on top of the mcsg C ABI.
+//
+// A maintainer of the reference (proj/, C++20) includes this header and links
+// libmcsg.so; nothing else in the reference changes. It converts the
+// reference's types at the boundary:
+//
+//   mcs::Graph (graph.hpp:31-62)         -> mcsg_graph (n*n codes, labels)
+//   mcs::SolveConfig (solve.hpp:118-125) -> mcsg_options
+//   mcsg_result                          -> mcs::SolveResult (solve.hpp:57-66)
+//
+// and raises mcs::GraphError where the C ABI reports MCSG_ERROR, as the
+// reference does (solve.cpp:94, portfolio.cpp:75). Timeout and cancellation
+// stay statuses. SolveConfig::visitor has no GPU counterpart (per-node host
+// callbacks cannot run inside the kernel) and is rejected.
+#pragma once
+
+#include <atomic>
+#include <chrono>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mcs/graph.hpp"
+#include "mcs/heuristics.hpp"
+#include "mcs/solve.hpp"
+#include "mcsg.h"
+
+namespace mcs::gpu {
+
+struct GraphBuffer {
+    std::vector<uint8_t> codes;
+    std::vector<int32_t> labels;
+    mcsg_graph view{};
+
+    explicit GraphBuffer(const Graph& g) {
+        const int n = g.n();
+        codes.resize(size_t(n) * size_t(n));
+        for (int u = 0; u < n; ++u)
+            for (int v = 0; v < n; ++v) codes[size_t(u) * n + v] = g.code(u, v);
+        view.n = n;
+        view.flags = (g.directed() ? MCSG_DIRECTED : 0u) | (g.labeled() ? MCSG_LABELED : 0u);
+        view.codes = codes.data();
+        if (g.labeled()) {
+            labels.assign(g.labels()->begin(), g.labels()->end());
+            view.labels = labels.data();
+        }
+    }
+};
+
+inline mcsg_options to_options(const SolveConfig& cfg, int mode) {
+    if (cfg.visitor) throw GraphError("mcs::gpu: NodeVisitor hooks are not supported on the GPU engine");
+    mcsg_options o{};
+    o.budget_s = cfg.budget_seconds;
+    o.order = static_cast<int32_t>(cfg.order);
+    o.mode = mode;
+    o.disable_pruning = cfg.disable_pruning ? 1 : 0;
+    o.floor_size = cfg.shared_bound ? static_cast<int32_t>(cfg.shared_bound->get()) : 0;
+    o.device = -1;
+    o.cancel = nullptr;  // set by CancelBridge when cfg.cancel is given
+    return o;
+}
+
+// SolveConfig::cancel is a std::atomic<bool>; the ABI polls an int32. A small
+// watcher thread mirrors one into the other for the duration of a call.
+class CancelBridge {
+public:
+    CancelBridge(const std::atomic<bool>* src, mcsg_options& o) : src_(src) {
+        if (!src_) return;
+        o.cancel = &flag_;
+        watcher_ = std::thread([this] {
+            while (!done_.load()) {
+                if (src_->load()) flag_ = 1;
+                std::this_thread::sleep_for(std::chrono::microseconds(200));
+            }
+        });
+    }
+    ~CancelBridge() {
+        done_.store(true);
+        if (watcher_.joinable()) watcher_.join();
+    }
+
+private:
+    const std::atomic<bool>* src_;
+    volatile int32_t flag_ = 0;
+    std::atomic<bool> done_{false};
+    std::thread watcher_;
+};
+
+inline SolveResult to_result(const mcsg_result& r, const mcsg_stats& st) {
+    SolveResult out;
+    out.status = r.status == MCSG_TIMEOUT     ? SolveStatus::timeout
+                 : r.status == MCSG_CANCELLED ? SolveStatus::cancelled
+                                              : SolveStatus::optimal;
+    out.size = r.size;
+    for (int k = 0; k < r.size; ++k) out.best.push_back({r.pairs[2 * k], r.pairs[2 * k + 1]});
+    out.stats.recursions = r.nodes;
+    out.stats.wall_seconds = st.wall_s;
+    out.stats.probes = st.probes;
+    return out;
+}
+
+inline void check(int32_t rc) {
+    if (rc == MCSG_ERROR) throw GraphError(std::string("mcs::gpu: ") + mcsg_last_error());
+}
+
+// mcs::solve (solve.hpp:128). MCSG_MODE_PARITY reproduces the reference's
+// node order and stats.recursions; the default is the all-warp engine.
+inline SolveResult solve(const Graph& g, const Graph& h, const SolveConfig& cfg = {},
+                         int mode = MCSG_MODE_THROUGHPUT) {
+    GraphBuffer gb(g), hb(h);
+    mcsg_options o = to_options(cfg, mode);
+    CancelBridge bridge(cfg.cancel, o);
+    mcsg_result r{};
+    mcsg_stats st{};
+    check(mcsg_solve(&gb.view, &hb.view, &o, &r, &st));
+    if (cfg.shared_bound) cfg.shared_bound->bump(r.size);
+    return to_result(r, st);
+}
+
+// mcs::solve_goal_directed (solve.hpp:132).
+inline SolveResult solve_goal_directed(const Graph& g, const Graph& h, const SolveConfig& cfg = {}) {
+    GraphBuffer gb(g), hb(h);
+    mcsg_options o = to_options(cfg, MCSG_MODE_THROUGHPUT);
+    CancelBridge bridge(cfg.cancel, o);
+    mcsg_result r{};
+    mcsg_stats st{};
+    check(mcsg_solve_goal_directed(&gb.view, &hb.view, &o, &r, &st));
+    return to_result(r, st);
+}
+
+// mcs::bound_jump_search (heuristics.hpp:69).
+inline SolveResult bound_jump_search(const Graph& g, const Graph& h, int current_best, JumpMode mode,
+                                     const SolveConfig& cfg = {}) {
+    GraphBuffer gb(g), hb(h);
+    mcsg_options o = to_options(cfg, MCSG_MODE_THROUGHPUT);
+    CancelBridge bridge(cfg.cancel, o);
+    mcsg_result r{};
+    mcsg_stats st{};
+    check(mcsg_bound_jump(&gb.view, &hb.view, current_best, mode == JumpMode::doubling ? 1 : 0, &o,
+                          &r, &st));
+    return to_result(r, st);
+}
+
+// oracle::verify (oracle.hpp:16) through the library's host verifier.
+inline bool verify(const Graph& g, const Graph& h, const Mapping& m) {
+    GraphBuffer gb(g), hb(h);
+    std::vector<int32_t> pairs;
+    for (const VtxPair& p : m) {
+        pairs.push_back(p.v);
+        pairs.push_back(p.u);
+    }
+    const int32_t rc = mcsg_verify(&gb.view, &hb.view, pairs.data(), int32_t(m.size()));
+    if (rc < 0) throw GraphError(std::string("verify: ") + mcsg_last_error());
+    return rc == 1;
+}
+
+}  // namespace mcs::gpu
