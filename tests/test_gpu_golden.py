@@ -1,0 +1,86 @@
+"""Full-size parity: GPU optima against the reference's own results.
+
+c2_sizes.json: all 100 C2 pairs (n=30) solved to optimality by the reference
+thread pool (oracle/_ref solve_parallel); c5_sample.json: 300 C5 pairs
+(n=16..24) by the reference sequential solve(), with node counts. The GPU
+must return the identical optimum for every pair (integer: exact), a mapping
+that verifies, and — in parity mode — the identical node count.
+"""
+import json
+import os
+
+import pytest
+
+import oracle as O
+import paper_1908_06418_b200 as M
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def c2_pairs():
+    out = []
+    for i in range(100):
+        k, j = i % 3, i // 3
+        s = 30000 + 1000 * k + 2 * j
+        p = (0.1, 0.3, 0.5)[k]
+        out.append((M.random_graph(30, p, s), M.random_graph(30, p, s + 1)))
+    return out
+
+
+def test_c2_batch_matches_reference_pool():
+    gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))
+    pairs = c2_pairs()
+    res, st = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    for i, ((g, h), r) in enumerate(zip(pairs, res)):
+        assert r.status == M.SolveStatus.optimal
+        assert r.size == gold["sizes"][str(i)], i
+        assert M.verify(g, h, r.best)
+    assert st.busy_cycles > 0
+
+
+def test_c5_sample_matches_reference_sizes_and_nodes():
+    gold = json.load(open(os.path.join(HERE, "golden", "c5_sample.json")))["pairs"]
+    pairs = []
+    for rec in gold:
+        i, n, p = rec["i"], rec["n"], rec["p"]
+        pairs.append((M.random_graph(n, p, 50000 + 2 * i), M.random_graph(n, p, 50001 + 2 * i)))
+    res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    for rec, (g, h), r in zip(gold, pairs, res):
+        assert r.status == M.SolveStatus.optimal and r.size == rec["size"], rec
+        assert M.verify(g, h, r.best)
+    # parity mode on the cheaper half: node counts equal the reference's stats.recursions
+    cheap = [k for k, rec in enumerate(gold) if rec["nodes"] < 2_000_000]
+    res, _ = M.solve_batch([pairs[k] for k in cheap], M.SolveConfig(mode=M.MODE_PARITY))
+    for k, r in zip(cheap, res):
+        assert (r.size, r.stats.recursions) == (gold[k]["size"], gold[k]["nodes"]), gold[k]
+
+
+def test_directed_labelled_n40_batch_against_oracle():
+    # C3 shape; the CPU oracle proves the cells it can in its budget
+    pairs, expect = [], []
+    for i, (L, p) in enumerate([(8, 0.5), (8, 0.3), (4, 0.5), (4, 0.3), (8, 0.1), (2, 0.5)]):
+        g = M.random_graph(40, p, 40000 + 2 * i, True, L)
+        h = M.random_graph(40, p, 40001 + 2 * i, True, L)
+        o = O.solve(O.G(40, g.codes.copy(), True, g.labels.copy()), O.G(40, h.codes.copy(), True, h.labels.copy()),
+                    budget=20)
+        if o.status == 0:
+            pairs.append((g, h))
+            expect.append(o.size)
+    assert pairs
+    res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    for (g, h), r, e in zip(pairs, res, expect):
+        assert r.status == M.SolveStatus.optimal and r.size == e and M.verify(g, h, r.best)
+
+
+def test_c4_hard_pair_two_independent_modes():
+    """C4 (n=45, p=0.5, seeds 45000/45001): the reference pool does not prove
+    it in 30 min (incumbent 16). Two independent GPU searches must
+    agree: the all-warp solve, and goal probes (16 reachable, 17 not)."""
+    g, h = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
+    r = M.solve(g, h, M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=300))
+    assert r.status == M.SolveStatus.optimal and M.verify(g, h, r.best)
+    assert r.size >= 16  # the reference pool's incumbent after 1800 s
+    jr = M.bound_jump_search(g, h, r.size, M.JumpMode.plus_one,
+                             M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=300))
+    assert jr.status == M.SolveStatus.optimal and jr.size == r.size and M.verify(g, h, jr.best)
