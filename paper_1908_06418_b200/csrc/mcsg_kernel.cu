@@ -30,7 +30,7 @@
 namespace mcsg {
 
 template <typename W, bool DIR, bool PAR>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 5))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
     mcs_search_kernel(KernelParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using Sm = WarpSmem<W, DIR>;

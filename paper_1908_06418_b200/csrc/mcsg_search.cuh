@@ -179,6 +179,10 @@ struct Search {
     W L[S], R[S];
     W LX[S];        // L with the branching vertex v removed
     int lc[S][P];   // |LX ∩ part_q(v)|
+    bool two = false;  // 64-bit kernel: the level has classes in the second slot (nc > 32)
+
+    // slot k holds live classes (slot 0 always; slot 1 only when nc > 32)
+    __device__ __forceinline__ bool live(int k) const { return k == 0 || two; }
 
     // The 32-bit kernel never spills: the host sizes its shared stack to the
     // path bound m(m+1)/2. The 64-bit kernel keeps levels past `cap` in HBM;
@@ -195,6 +199,7 @@ struct Search {
 
     template <typename Ptr>
     __device__ __forceinline__ void load_from(const Ptr* p, int nc) {
+        two = S > 1 && nc > 32;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             const int c = lane + 32 * k;
@@ -289,6 +294,11 @@ struct Search {
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             LX[k] = L[k] & ~vb;
+            if (!live(k)) {
+#pragma unroll
+                for (int q = 0; q < P; ++q) lc[k][q] = 0;
+                continue;
+            }
             if constexpr (!DIR) {
                 const int a = Bits<W>::popc(LX[k] & g[1]);
                 lc[k][1] = a;
@@ -306,6 +316,7 @@ struct Search {
         unsigned sm = 0;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
+            if (!live(k)) continue;
             const W rx = R[k] & ~ub;
             if constexpr (!DIR) {
                 const int b = Bits<W>::popc(rx & h[1]);
@@ -335,6 +346,7 @@ struct Search {
         unsigned key = kNoKey;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
+            if (!live(k)) continue;
             const W rx = R[k] & ~ub;
 #pragma unroll
             for (int pp = 0; pp < P; ++pp) {
