@@ -83,6 +83,15 @@ typedef struct mcsg_options {
     int32_t smem_classes;           /* 0 = auto: class-stack entries per warp in smem */
     uint64_t seed;                  /* restarts:<seed> portfolio member: donation order */
     const volatile int32_t* cancel; /* SolveConfig::cancel; polled by the kernel */
+    /* Multi-GPU (one process drives every device; incumbent sizes travel over
+     * NVLink P2P). n_devices > 1: mcsg_solve shards ONE instance — the host
+     * expands the top of the tree into `frontier` subtrees per device, dealt
+     * round-robin — and mcsg_portfolio spreads its members over the devices
+     * (first member to finish proves for all). Repeated ordinals are allowed
+     * (shards then run one after another on that device). */
+    int32_t n_devices;
+    int32_t devices[16];
+    int32_t frontier;               /* subtrees per device, 0 = 256 */
 } mcsg_options;
 
 typedef struct mcsg_stats {

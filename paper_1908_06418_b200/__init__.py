@@ -95,7 +95,8 @@ class _Options(C.Structure):
     _fields_ = [("budget_s", C.c_double), ("order", C.c_int32), ("mode", C.c_int32),
                 ("goal", C.c_int32), ("disable_pruning", C.c_int32), ("floor_size", C.c_int32),
                 ("device", C.c_int32), ("max_warps", C.c_int32), ("smem_classes", C.c_int32),
-                ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32))]
+                ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32)),
+                ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -370,6 +371,8 @@ class SolveConfig:
     max_warps: int = 0
     smem_classes: int = 0
     seed: int = 0
+    devices: tuple = ()                # > 1 entry: shard one instance over these GPUs
+    frontier: int = 0                  # host-expanded subtrees per device (0 = 256)
 
 
 @dataclass
@@ -426,6 +429,12 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
     o.seed = cfg.seed
     if cfg.cancel is not None:
         o.cancel = C.cast(C.pointer(cfg.cancel), C.POINTER(C.c_int32))
+    if len(cfg.devices) > 16:
+        raise GraphError("at most 16 devices")
+    o.n_devices = len(cfg.devices)
+    for i, dv in enumerate(cfg.devices):
+        o.devices[i] = int(dv)
+    o.frontier = cfg.frontier
     for k, v in over.items():
         setattr(o, k, v)
     return o

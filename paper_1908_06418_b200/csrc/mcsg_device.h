@@ -122,6 +122,8 @@ struct Ctl {
     Line32 next_root;  // root tasks are implicit: instance ids handed out by atomicAdd
 };
 
+constexpr int kMaxPeers = 16;
+
 struct KernelParams {
     const InstanceDesc* inst;
     InstanceState* ist;
@@ -130,6 +132,13 @@ struct KernelParams {
     Ctl* ctl;
     uint32_t cap_mask;       // ring capacity - 1 (power of two)
     int32_t n_inst;
+    int32_t n_roots;         // instances handed out as root tasks (0: the ring was pre-seeded)
+    // Cross-device incumbent of group 0 (one instance sharded over devices, or
+    // portfolio members on different devices): other devices' GroupState,
+    // reachable over NVLink P2P. Sizes are pushed with system-scope atomicMax.
+    GroupState* peer_grp[kMaxPeers];
+    int32_t n_peers;
+    int32_t peer_done_on_complete;  // portfolio: the first device to finish proves for all
     const volatile int32_t* cancel;  // host-mapped cancel flag (may be null)
     unsigned long long budget_ns;    // per-warp deadline = warp start + budget, 0 = none
     uint64_t* spill;         // per-warp HBM spill area for class levels (64-bit kernel only)

@@ -21,6 +21,7 @@
 
 #include "../../include/mcsg.h"
 #include "mcsg_device.h"
+#include "mcsg_frontier.hpp"
 #include "mcsg_graph.hpp"
 
 namespace mcsg {
@@ -123,15 +124,18 @@ struct Context {
 };
 
 std::mutex g_ctx_mu;
-std::map<int, std::unique_ptr<Context>> g_ctx;
+std::map<std::pair<int, int>, std::unique_ptr<Context>> g_ctx;
 
-Context& context(int device) {
+// Device context `slot` of a CUDA device. Slot > 0 only appears when several
+// shards of one multi-device solve are placed on the same physical device
+// (each shard needs its own ring and instance state).
+Context& context(int device, int slot = 0) {
     int dev = device;
     if (dev < 0) {
         ck(cudaGetDevice(&dev), "cudaGetDevice");
     }
     std::lock_guard<std::mutex> lock(g_ctx_mu);
-    auto it = g_ctx.find(dev);
+    auto it = g_ctx.find({dev, slot});
     if (it != g_ctx.end()) return *it->second;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
@@ -139,7 +143,7 @@ Context& context(int device) {
     if (dev >= count) throw Error("CUDA device " + std::to_string(dev) + " does not exist");
     auto ctx = std::make_unique<Context>(dev);
     Context& ref = *ctx;
-    g_ctx[dev] = std::move(ctx);
+    g_ctx[{dev, slot}] = std::move(ctx);
     return ref;
 }
 
@@ -219,26 +223,38 @@ double secs_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-// The single launch path shared by every entry point.
-LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
-    Context& ctx = context(o.device);
-    std::lock_guard<std::mutex> lock(ctx.mu);
-    ck(cudaSetDevice(ctx.device), "cudaSetDevice");
-    LaunchOut out;
-    const int n = int(jobs.size());
-    out.jobs.resize(n);
-    out.groups.resize(n_groups);
-    if (n == 0) return out;
+// What a launch does beyond "every instance is a root task".
+struct LaunchExtras {
+    std::vector<TaskSlot> seeded;    // subtrees published in the ring before the launch
+    bool roots = true;               // hand out every instance as a root task
+    std::vector<GroupState*> peers;  // group 0's incumbent on the other devices (P2P)
+    bool peer_done_on_complete = false;
+    bool relabeled = false;          // jobs already in the kernel's vertex order
+    int seed_best = 0;               // host incumbent of instance 0 (frontier expansion)
+    std::vector<uint8_t> seed_v, seed_u;
+};
 
+// A launch in flight on one context (ctx.mu held by the caller until finish()).
+struct InFlight {
+    Context* ctx = nullptr;
+    std::vector<Job>* jobs = nullptr;
+    mcsg_options o{};
+    int n = 0, n_groups = 0, ctas = 0, warps = 0, smem_classes = 0;
     bool wide = false, directed = false;
+    size_t seeded = 0;
+    std::chrono::steady_clock::time_point t_stage;
+    double h2d_s = 0;
+};
+
+// Kernel shape for a batch: specialisation, shared-memory class stack, grid.
+void plan(Context& ctx, const std::vector<Job>& jobs, const mcsg_options& o, InFlight* f) {
+    f->wide = false;
+    f->directed = false;
     for (const Job& j : jobs) {
-        wide |= std::max(j.g.n, j.h.n) > 32;
-        directed |= j.g.directed;
+        f->wide |= std::max(j.g.n, j.h.n) > 32;
+        f->directed |= j.g.directed;
     }
     const bool parity = o.mode == MCSG_MODE_PARITY;
-    if (!parity)
-        for (Job& j : jobs) relabel_for_throughput(j);
-
     // Shared-memory class stack. A search level at depth d holds at most
     // min(n_G, n_H) - d classes, so m(m+1)/2 (+ one level of slack) bounds the
     // whole path: the 32-bit kernel never spills. The 64-bit kernel takes
@@ -247,46 +263,83 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     for (const Job& j : jobs) maxm = std::max(maxm, std::min(j.g.n, j.h.n));
     const int path_bound = maxm * (maxm + 1) / 2 + 2 * kMaxN;
     int smem_classes = o.smem_classes;
-    int blocks = kernel_occupancy(wide, directed, 64);
+    int blocks = kernel_occupancy(f->wide, f->directed, 64);
     if (blocks <= 0) throw Error("search kernel cannot be resident on this device");
     if (smem_classes <= 0) {
         const int per_cta = ctx.smem_per_sm / blocks - 1024;
         const int per_warp = per_cta / kWarpsPerCta;
-        const int fixed = kernel_smem_per_warp(wide, directed, 0);
-        smem_classes = std::clamp((per_warp - fixed) / (wide ? 16 : 8), 64, 2048);
+        const int fixed = kernel_smem_per_warp(f->wide, f->directed, 0);
+        smem_classes = std::clamp((per_warp - fixed) / (f->wide ? 16 : 8), 64, 2048);
         smem_classes = std::min(smem_classes, path_bound);
-        while (smem_classes > 64 && kernel_occupancy(wide, directed, smem_classes) < blocks)
+        while (smem_classes > 64 && kernel_occupancy(f->wide, f->directed, smem_classes) < blocks)
             smem_classes -= 16;
     }
     smem_classes = std::max(smem_classes, 64);
-    if (!wide) smem_classes = std::max(smem_classes, path_bound);  // 32-bit kernel: no spill path
-    blocks = kernel_occupancy(wide, directed, smem_classes);
+    if (!f->wide) smem_classes = std::max(smem_classes, path_bound);  // 32-bit kernel: no spill path
+    blocks = kernel_occupancy(f->wide, f->directed, smem_classes);
     if (blocks <= 0) throw Error("requested shared-memory class stack does not fit");
     int ctas = blocks * ctx.sms;
     if (o.max_warps > 0) ctas = std::min(ctas, (o.max_warps + kWarpsPerCta - 1) / kWarpsPerCta);
-    if (parity) ctas = std::min(ctas, (n + kWarpsPerCta - 1) / kWarpsPerCta);
-    ctas = std::max(ctas, 1);
-    const int warps = ctas * kWarpsPerCta;
-    ctx.reserve(size_t(n), size_t(n_groups), size_t(warps));
+    if (parity) ctas = std::min(ctas, (int(jobs.size()) + kWarpsPerCta - 1) / kWarpsPerCta);
+    f->ctas = std::max(ctas, 1);
+    f->warps = f->ctas * kWarpsPerCta;
+    f->smem_classes = smem_classes;
+}
 
-    auto t_stage = std::chrono::steady_clock::now();
+// Packs, stages and launches; returns without waiting.
+InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_options& o,
+               const LaunchExtras& ex) {
+    ck(cudaSetDevice(ctx.device), "cudaSetDevice");
+    InFlight f;
+    f.ctx = &ctx;
+    f.jobs = &jobs;
+    f.o = o;
+    f.n = int(jobs.size());
+    f.n_groups = n_groups;
+    const bool parity = o.mode == MCSG_MODE_PARITY;
+    if (!parity && !ex.relabeled)
+        for (Job& j : jobs) relabel_for_throughput(j);
+    plan(ctx, jobs, o, &f);
+    const int n = f.n;
+    ctx.reserve(size_t(n), size_t(n_groups), size_t(f.warps));
+    if (ex.seeded.size() + size_t(f.warps) > kRingCap) throw Error("too many seeded subtrees for the ring");
+
+    f.t_stage = std::chrono::steady_clock::now();
     for (int i = 0; i < n; ++i) {
         pack_instance(jobs[i].g, jobs[i].h, jobs[i].goal, o.disable_pruning == 0, jobs[i].floor_size,
                       jobs[i].group, &ctx.h_inst[i]);
         std::memset(&ctx.h_ist[i], 0, sizeof(InstanceState));
-        ctx.h_ist[i].open_tasks = 1;
+        ctx.h_ist[i].open_tasks = ex.roots ? 1 : 0;
     }
     for (int gi = 0; gi < n_groups; ++gi) {
         ctx.h_grp[gi] = GroupState{};
         ctx.h_grp[gi].winner = -1;
     }
+    if (n > 0 && ex.seed_best > 0) {  // the host's incumbent travels with the shard
+        InstanceState& s0 = ctx.h_ist[0];
+        s0.map_size = unsigned(ex.seed_best);
+        for (int k = 0; k < ex.seed_best; ++k) s0.map_v[k] = ex.seed_v[k], s0.map_u[k] = ex.seed_u[k];
+        ctx.h_grp[0].best = unsigned(ex.seed_best);
+    }
+    for (const TaskSlot& t : ex.seeded) ctx.h_ist[t.hdr.inst].open_tasks += 1;
     ck(cudaMemcpyAsync(ctx.d_inst, ctx.h_inst, sizeof(InstanceDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_ist, ctx.h_ist, sizeof(InstanceState) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_grp, ctx.h_grp, sizeof(GroupState) * n_groups, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     *ctx.h_ctl = Ctl{};
-    ctx.h_ctl->pending.v = n;
+    ctx.h_ctl->pending.v = (ex.roots ? n : 0) + int(ex.seeded.size());
+    ctx.h_ctl->tail.v = ex.seeded.size();
     ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
+    if (!ex.seeded.empty()) {
+        // published slots: sequence word = ticket + 1 (the consumer of ticket i reads it)
+        std::vector<TaskSlot> staged(ex.seeded);
+        for (size_t i = 0; i < staged.size(); ++i) staged[i].seq = i + 1;
+        ck(cudaMemcpyAsync(ctx.d_slots, staged.data(), sizeof(TaskSlot) * staged.size(),
+                           cudaMemcpyHostToDevice, ctx.stream),
+           "h2d seeded tasks");
+        ck(cudaStreamSynchronize(ctx.stream), "h2d seeded tasks");  // `staged` is pageable
+    }
+    f.seeded = ex.seeded.size();
     *ctx.h_cancel = 0;
 
     KernelParams p{};
@@ -297,28 +350,43 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     p.ctl = ctx.d_ctl;
     p.cap_mask = kRingCap - 1;
     p.n_inst = n;
+    p.n_roots = ex.roots ? n : 0;
+    p.n_peers = int(ex.peers.size());
+    if (p.n_peers > kMaxPeers) throw Error("too many peer devices");
+    for (int q = 0; q < p.n_peers; ++q) p.peer_grp[q] = ex.peers[q];
+    p.peer_done_on_complete = ex.peer_done_on_complete ? 1 : 0;
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
     p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
     p.spill = ctx.d_spill;
-    p.spill_classes = wide ? kSpillClasses : 0;
-    p.smem_classes = smem_classes;
+    p.spill_classes = f.wide ? kSpillClasses : 0;
+    p.smem_classes = f.smem_classes;
     p.donate = parity ? 0 : 1;
     p.poll_interval = parity ? 4096 : 256;
     p.counters = ctx.d_cnt;
 
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
-    ck(kernel_launch(wide, directed, parity, p, ctas, ctx.stream), "search kernel launch");
+    ck(kernel_launch(f.wide, f.directed, parity, p, f.ctas, ctx.stream), "search kernel launch");
     ck(cudaEventRecord(ctx.ev1, ctx.stream), "event");
     ck(cudaMemcpyAsync(ctx.h_ist, ctx.d_ist, sizeof(InstanceState) * n, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_grp, ctx.d_grp, sizeof(GroupState) * n_groups, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_cnt, ctx.d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
-    Ctl* ctl_out = ctx.h_ctl;
-    ck(cudaMemcpyAsync(ctl_out, ctx.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
-    out.h2d_s = secs_since(t_stage);
-    if (o.cancel) {
+    ck(cudaMemcpyAsync(ctx.h_ctl, ctx.d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
+    f.h2d_s = secs_since(f.t_stage);
+    return f;
+}
+
+// Waits for a launch and unpacks its results.
+LaunchOut finish(InFlight& f) {
+    Context& ctx = *f.ctx;
+    ck(cudaSetDevice(ctx.device), "cudaSetDevice");
+    LaunchOut out;
+    const int n = f.n, n_groups = f.n_groups;
+    out.jobs.resize(n);
+    out.groups.resize(n_groups);
+    if (f.o.cancel) {
         // mirror the caller's flag into host-mapped memory the kernel polls
         while (cudaStreamQuery(ctx.stream) == cudaErrorNotReady) {
-            if (*o.cancel) *reinterpret_cast<volatile int32_t*>(ctx.h_cancel) = 1;
+            if (*f.o.cancel) *reinterpret_cast<volatile int32_t*>(ctx.h_cancel) = 1;
             std::this_thread::sleep_for(std::chrono::microseconds(50));
         }
     }
@@ -326,19 +394,20 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1);
     out.kernel_s = ms * 1e-3;
+    out.h2d_s = f.h2d_s;
     out.counters = *ctx.h_cnt;
-    out.warps = warps;
-    out.ctas = ctas;
-    out.smem_per_cta = kernel_smem_per_warp(wide, directed, smem_classes) * kWarpsPerCta;
-    out.smem_classes = smem_classes;
+    out.warps = f.warps;
+    out.ctas = f.ctas;
+    out.smem_per_cta = kernel_smem_per_warp(f.wide, f.directed, f.smem_classes) * kWarpsPerCta;
+    out.smem_classes = f.smem_classes;
     out.h2d_bytes = (sizeof(InstanceDesc) + sizeof(InstanceState)) * uint64_t(n) +
-                    sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl);
+                    sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl) + sizeof(TaskSlot) * f.seeded;
     out.d2h_bytes = sizeof(InstanceState) * uint64_t(n) + sizeof(GroupState) * uint64_t(n_groups) +
                     sizeof(Counters) + sizeof(Ctl);
     out.launches = 2;  // ring reset + search kernel
     if (out.counters.overflow) throw Error("class stack overflow (internal error)");
 
-    const int stop = ctl_out->stop.v;
+    const int stop = ctx.h_ctl->stop.v;
     for (int gi = 0; gi < n_groups; ++gi) {
         out.groups[gi].done = ctx.h_grp[gi].done != 0;
         out.groups[gi].winner = ctx.h_grp[gi].winner;
@@ -347,7 +416,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
     for (int i = 0; i < n; ++i) {
         const InstanceState& s = ctx.h_ist[i];
         JobResult& r = out.jobs[i];
-        const Job& j = jobs[i];
+        const Job& j = (*f.jobs)[i];
         r.completed = s.open_tasks == 0;
         r.nodes = s.nodes;
         r.size = int(s.map_size);
@@ -367,6 +436,157 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
         }
     }
     return out;
+}
+
+// The single-device launch path shared by every entry point.
+LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
+    if (jobs.empty()) {
+        LaunchOut out;
+        out.groups.resize(n_groups);
+        return out;
+    }
+    Context& ctx = context(o.device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    InFlight f = start(ctx, jobs, n_groups, o, LaunchExtras{});
+    return finish(f);
+}
+
+// ------------------------------------------------------------ multi-device --
+// One launch per device; `members[i]` are the instances placed on device i
+// (all in group 0). Contexts are locked in a fixed order, peer access is
+// enabled between distinct physical devices, and every device gets the other
+// devices' GroupState (group 0) as incumbent peers.
+struct DevicePlan {
+    int device = 0;
+    std::vector<Job> jobs;
+    std::vector<TaskSlot> seeded;
+    bool roots = true;
+};
+
+std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_options& o,
+                                    bool peer_done_on_complete, int seed_best,
+                                    const std::vector<uint8_t>& seed_v, const std::vector<uint8_t>& seed_u) {
+    const int D = int(plans.size());
+    std::vector<Context*> ctxs(D);
+    std::map<int, int> used;
+    for (int i = 0; i < D; ++i) ctxs[i] = &context(plans[i].device, used[plans[i].device]++);
+    std::vector<Context*> order(ctxs);
+    std::sort(order.begin(), order.end());
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (Context* c : order) locks.emplace_back(c->mu);
+    // peer access between distinct physical devices
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            const int a = ctxs[i]->device, b = ctxs[j]->device;
+            if (a == b) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can)
+                throw Error("devices " + std::to_string(a) + " and " + std::to_string(b) +
+                            " cannot access each other (no P2P)");
+            ck(cudaSetDevice(a), "cudaSetDevice");
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    // allocate every device's state first so that peer pointers exist
+    for (int i = 0; i < D; ++i) {
+        InFlight shape;
+        mcsg_options oo = o;
+        oo.mode = MCSG_MODE_THROUGHPUT;
+        plan(*ctxs[i], plans[i].jobs, oo, &shape);
+        ck(cudaSetDevice(ctxs[i]->device), "cudaSetDevice");
+        ctxs[i]->reserve(plans[i].jobs.size(), 1, size_t(shape.warps));
+    }
+    std::vector<InFlight> fl(D);
+    for (int i = 0; i < D; ++i) {
+        LaunchExtras ex;
+        ex.seeded = plans[i].seeded;
+        ex.roots = plans[i].roots;
+        ex.relabeled = true;
+        ex.peer_done_on_complete = peer_done_on_complete;
+        for (int j = 0; j < D; ++j)
+            if (j != i) ex.peers.push_back(ctxs[j]->d_grp);
+        ex.seed_best = seed_best;
+        ex.seed_v = seed_v;
+        ex.seed_u = seed_u;
+        mcsg_options oo = o;
+        oo.mode = MCSG_MODE_THROUGHPUT;
+        oo.device = ctxs[i]->device;
+        fl[i] = start(*ctxs[i], plans[i].jobs, 1, oo, ex);
+    }
+    std::vector<LaunchOut> out(D);
+    for (int i = 0; i < D; ++i) out[i] = finish(fl[i]);
+    return out;
+}
+
+// One instance sharded over devices (SURVEY §8(e) "sharded" mode).
+JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_options& o, LaunchOut* agg,
+                        uint64_t* host_nodes) {
+    const int D = o.n_devices;
+    Job job = make_job(G, H, o.order);
+    job.goal = o.goal;
+    job.floor_size = o.floor_size;
+    job.group = 0;
+    relabel_for_throughput(job);
+    InstanceDesc desc;
+    pack_instance(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, &desc);
+    const int per_dev = o.frontier > 0 ? o.frontier : 256;
+    Frontier fr = expand_frontier(desc, job.g.directed, per_dev * D, 0);
+    *host_nodes = fr.nodes;
+    auto host_result = [&](bool optimal_by_host) {
+        JobResult r;
+        r.status = MCSG_OPTIMAL;
+        r.size = fr.best_size;
+        r.completed = optimal_by_host;
+        for (int k = 0; k < fr.best_size; ++k) {
+            r.pairs.push_back(job.inv_g.empty() ? fr.best_v[k] : job.inv_g[fr.best_v[k]]);
+            r.pairs.push_back(job.inv_h.empty() ? fr.best_u[k] : job.inv_h[fr.best_u[k]]);
+        }
+        r.nodes = fr.nodes;
+        return r;
+    };
+    if (fr.max_reached || fr.tasks.empty()) return host_result(true);  // the host already finished
+    std::vector<DevicePlan> plans(D);
+    for (int i = 0; i < D; ++i) {
+        plans[i].device = o.devices[i];
+        plans[i].jobs.push_back(job);
+        plans[i].roots = false;
+    }
+    for (size_t k = 0; k < fr.tasks.size(); ++k) plans[k % D].seeded.push_back(fr.tasks[k]);
+    std::vector<LaunchOut> outs = launch_multi(plans, o, false, fr.best_size, fr.best_v, fr.best_u);
+    JobResult best = host_result(false);
+    bool all_complete = true, any_done_max = false;
+    int status = MCSG_OPTIMAL;
+    uint64_t nodes = fr.nodes;
+    for (const LaunchOut& lo : outs) {
+        const JobResult& r = lo.jobs[0];
+        nodes += r.nodes;
+        all_complete &= r.completed;
+        any_done_max |= lo.groups[0].done && !r.completed;  // stopped early because the max was reached
+        if (r.size > best.size) best = r;
+        if (r.status != MCSG_OPTIMAL) status = r.status;
+        best.solve_s = std::max(best.solve_s, r.solve_s);
+    }
+    best.nodes = nodes;
+    best.status = (all_complete || any_done_max) ? MCSG_OPTIMAL : status;
+    // aggregate counters for the stats record
+    *agg = outs[0];
+    agg->kernel_s = 0;
+    for (const LaunchOut& lo : outs) agg->kernel_s = std::max(agg->kernel_s, lo.kernel_s);
+    for (size_t i = 1; i < outs.size(); ++i) {
+        agg->counters.nodes += outs[i].counters.nodes;
+        agg->counters.splits += outs[i].counters.splits;
+        agg->counters.donations += outs[i].counters.donations;
+        agg->counters.tasks += outs[i].counters.tasks;
+        agg->counters.busy_cycles += outs[i].counters.busy_cycles;
+        agg->counters.idle_cycles += outs[i].counters.idle_cycles;
+        agg->warps += outs[i].warps;
+        agg->ctas += outs[i].ctas;
+        agg->h2d_bytes += outs[i].h2d_bytes;
+        agg->d2h_bytes += outs[i].d2h_bytes;
+        agg->launches += outs[i].launches;
+    }
+    return best;
 }
 
 void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probes) {
@@ -551,7 +771,28 @@ int32_t mcsg_solve_batch(int32_t count, const mcsg_graph* gs, const mcsg_graph* 
 
 int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
                    mcsg_result* out, mcsg_stats* stats) {
-    return mcsg_solve_batch(1, g, h, opt, out, stats);
+    const mcsg_options o = defaults(opt);
+    if (o.n_devices <= 1) return mcsg_solve_batch(1, g, h, opt, out, stats);
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (o.n_devices > 16) throw Error("at most 16 devices");
+        if (o.mode == MCSG_MODE_PARITY) throw Error("parity mode runs on one device");
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        LaunchOut agg;
+        uint64_t host_nodes = 0;
+        const JobResult r = solve_sharded(G, H, o, &agg, &host_nodes);
+        write_result(G, H, r, out);
+        fill_stats(stats, agg, secs_since(t0), 0);
+        if (stats) stats->nodes += host_nodes;
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
@@ -583,17 +824,61 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
         }
         mcsg_options lo_opt = o;
         lo_opt.mode = MCSG_MODE_THROUGHPUT;  // members share the incumbent size
-        LaunchOut lo = launch(jobs, 1, lo_opt);
+        std::vector<JobResult> members(count);
+        bool done = false;
+        int w = -1;
+        LaunchOut lo;
+        if (o.n_devices <= 1) {
+            lo = launch(jobs, 1, lo_opt);
+            members = lo.jobs;
+            done = lo.groups[0].done;
+            w = lo.groups[0].winner;
+        } else {
+            // members spread over the devices; the first to finish stops all (P2P done flag)
+            const int D = std::min<int>(o.n_devices, 16);
+            std::vector<DevicePlan> plans(D);
+            std::vector<std::vector<int>> index(D);
+            for (int d = 0; d < D; ++d) plans[d].device = o.devices[d];
+            for (int i = 0; i < count; ++i) {
+                plans[i % D].jobs.push_back(jobs[i]);
+                index[i % D].push_back(i);
+            }
+            for (int d = 0; d < D; ++d)
+                for (Job& j : plans[d].jobs) relabel_for_throughput(j);
+            std::vector<DevicePlan> used;
+            std::vector<std::vector<int>> used_index;
+            for (int d = 0; d < D; ++d)
+                if (!plans[d].jobs.empty()) used.push_back(std::move(plans[d])), used_index.push_back(index[d]);
+            std::vector<LaunchOut> outs = launch_multi(used, lo_opt, true, 0, {}, {});
+            double first = 1e300;
+            for (size_t d = 0; d < outs.size(); ++d) {
+                for (size_t k = 0; k < used_index[d].size(); ++k) members[used_index[d][k]] = outs[d].jobs[k];
+                if (outs[d].groups[0].done) {
+                    done = true;
+                    const int lw = outs[d].groups[0].winner;
+                    if (lw >= 0 && outs[d].jobs[lw].completed && outs[d].jobs[lw].solve_s < first) {
+                        first = outs[d].jobs[lw].solve_s;
+                        w = used_index[d][lw];
+                    }
+                }
+            }
+            lo = outs[0];
+            for (size_t d = 1; d < outs.size(); ++d) {
+                lo.counters.nodes += outs[d].counters.nodes;
+                lo.kernel_s = std::max(lo.kernel_s, outs[d].kernel_s);
+                lo.warps += outs[d].warps;
+                lo.launches += outs[d].launches;
+            }
+        }
         // best mapping among members (sizes are shared, mappings are per member)
         int bi = 0;
         for (int i = 1; i < count; ++i)
-            if (lo.jobs[i].size > lo.jobs[bi].size) bi = i;
-        JobResult r = lo.jobs[bi];
+            if (members[i].size > members[bi].size) bi = i;
+        JobResult r = members[bi];
         r.nodes = 0;
-        for (const auto& jr : lo.jobs) r.nodes += jr.nodes;
-        const int w = lo.groups[0].winner;
-        r.status = lo.groups[0].done ? MCSG_OPTIMAL : lo.jobs[bi].status;
-        if (w >= 0) r.solve_s = lo.jobs[w].solve_s;
+        for (const auto& jr : members) r.nodes += jr.nodes;
+        r.status = done ? MCSG_OPTIMAL : members[bi].status;
+        if (w >= 0) r.solve_s = members[w].solve_s;
         write_result(G, H, r, out);
         if (winner_out) *winner_out = w;
         fill_stats(stats, lo, secs_since(t0), 0);

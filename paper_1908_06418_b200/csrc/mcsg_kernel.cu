@@ -89,11 +89,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             int spins = 0;
             for (;;) {
                 if (!have_ticket) {
-                    int r = p.n_inst;
-                    if (lane == 0 && ld_volatile(&ctl->next_root.v) < p.n_inst)
+                    int r = p.n_roots;
+                    if (lane == 0 && ld_volatile(&ctl->next_root.v) < p.n_roots)
                         r = atomicAdd(&ctl->next_root.v, 1);
                     r = __shfl_sync(kFull, r, 0);
-                    if (r < p.n_inst) {
+                    if (r < p.n_roots) {
                         inst = r;
                         got = true;
                         break;
@@ -288,6 +288,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                     __threadfence();
                     atomicMax(&gs->best, unsigned(dd + 1));
                 }
+                // push the size to the other devices' incumbents (NVLink P2P)
+                if (grp == 0 && lane < p.n_peers) atomicMax_system(&p.peer_grp[lane]->best, unsigned(dd + 1));
             }
             __syncwarp();
             if (lane == 0) {
@@ -459,10 +461,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                             gs->reached = 1;
                             if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
                         }
+                        if (grp == 0 && lane < p.n_peers) {  // stop every device
+                            atomicExch_system(&p.peer_grp[lane]->reached, 1);
+                            atomicExch_system(&p.peer_grp[lane]->done, 1u);
+                        }
                         goto finish;
                     }
                     if (prune && goal == 0 && d + 1 >= maxp) {  // search_core.hpp:151-154
                         if (lane == 0 && atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
+                        if (grp == 0 && lane < p.n_peers) atomicExch_system(&p.peer_grp[lane]->done, 1u);
                         goto finish;
                     }
                 }
@@ -574,6 +581,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 if (left == 0) {
                     is->t_done_ns = globaltimer();
                     if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
+                    // portfolio across devices: a complete member search proves
+                    // the optimum for every member (portfolio.cpp:271-279)
+                    if (grp == 0 && p.peer_done_on_complete)
+                        for (int q = 0; q < p.n_peers; ++q) atomicExch_system(&p.peer_grp[q]->done, 1u);
                 }
                 atomicSub(&ctl->pending.v, 1);
             }
