@@ -138,12 +138,14 @@ int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
 int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best,
                         int32_t doubling, const mcsg_options* opt, mcsg_result* out,
                         mcsg_stats* stats);
-/* Races `count` member strategies (orderings / seeds) of ONE pair in one
- * launch with a shared incumbent size; first member to prove wins
- * (portfolio.cpp:249-292). orders[i] in MCSG_ORDER_*; winner_out may be NULL. */
+/* Races `count` member strategies of ONE pair in one launch with a shared
+ * incumbent size; first member to prove wins (portfolio.cpp:249-292).
+ * orders[i] in MCSG_ORDER_*; seeds[i] != 0 gives member i a seeded search
+ * order (the restarts:<seed> member); either array may be NULL; winner_out may
+ * be NULL. */
 int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
-                       const int32_t* orders, const mcsg_options* opt, mcsg_result* out,
-                       int32_t* winner_out, mcsg_stats* stats);
+                       const int32_t* orders, const uint64_t* seeds, const mcsg_options* opt,
+                       mcsg_result* out, int32_t* winner_out, mcsg_stats* stats);
 
 /* ---- graph core / loader ---------------------------------------------- */
 /* 1 valid, 0 invalid, MCSG_ERROR-style -1 on out-of-range vertices */

@@ -132,7 +132,7 @@ def lib():
         L.mcsg_solve_batch.argtypes = [C.c_int32, G, G, O, R, S]
         L.mcsg_solve_goal_directed.argtypes = [G, G, O, R, S]
         L.mcsg_bound_jump.argtypes = [G, G, C.c_int32, C.c_int32, O, R, S]
-        L.mcsg_portfolio.argtypes = [G, G, C.c_int32, P(C.c_int32), O, R, P(C.c_int32), S]
+        L.mcsg_portfolio.argtypes = [G, G, C.c_int32, P(C.c_int32), P(C.c_uint64), O, R, P(C.c_int32), S]
         L.mcsg_verify.argtypes = [G, G, P(C.c_int32), C.c_int32]
         L.mcsg_random_graph.argtypes = [C.c_int32, C.c_double, C.c_uint64, C.c_uint32, C.c_int32,
                                         P(C.c_uint8), P(C.c_int32)]
@@ -652,9 +652,10 @@ def run_portfolio(g: Graph, h: Graph, specs, config: SolveConfig | None = None) 
     if not specs:
         raise GraphError("portfolio needs at least one engine spec")
     orders = (C.c_int32 * len(specs))(*[int(s.order) for s in specs])
+    seeds = (C.c_uint64 * len(specs))(*[int(s.restart_seed or 0) for s in specs])
     r, st = _Result(), _Stats()
     win = C.c_int32(-1)
-    _check(lib().mcsg_portfolio(C.byref(g._c()), C.byref(h._c()), len(specs), orders,
+    _check(lib().mcsg_portfolio(C.byref(g._c()), C.byref(h._c()), len(specs), orders, seeds,
                                 C.byref(_options(config)), C.byref(r), C.byref(win), C.byref(st)))
     res = _result(r, st)
     return PortfolioResult(res.status, specs[win.value].name() if win.value >= 0 else "", res.size,

@@ -156,6 +156,7 @@ struct Job {
     int group = 0;
     int goal = 0;
     int floor_size = 0;
+    uint64_t seed = 0;         // throughput mode: seeded search order (restarts:<seed>)
 };
 
 struct JobResult {
@@ -203,20 +204,37 @@ Job make_job(const HostGraph& g, const HostGraph& h, int order) {
 // Throughput mode: relabel G so that its ids follow select_vertex's order
 // (degree desc, id asc; label_classes.cpp:69-78). The kernel then picks v with
 // one ctz; the composed permutation is undone on the returned mapping.
-void relabel_for_throughput(Job& j) {
+//
+// A nonzero seed is the GPU counterpart of the "restarts:<seed>" portfolio
+// member (restarts.cpp:213-228 draws the next segment with mt19937_64): it
+// diversifies the search order instead — equal-degree G vertices are ordered
+// by a seeded permutation and H is relabelled by random_permutation(n_H, seed),
+// so u candidates are tried in a seeded order. Optima are unaffected.
+void relabel_for_throughput(Job& j, uint64_t seed = 0) {
     const int n = j.g.n;
     std::vector<int> order(n);
     for (int v = 0; v < n; ++v) order[v] = v;
     std::vector<int> deg(n);
     for (int v = 0; v < n; ++v) deg[v] = j.g.degree(v);
+    std::vector<int> tie(n);
+    for (int v = 0; v < n; ++v) tie[v] = v;
+    if (seed) tie = random_permutation(n, seed * 0x9e3779b97f4a7c15ull);
     std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return deg[a] != deg[b] ? deg[a] > deg[b] : a < b; });
+                     [&](int a, int b) { return deg[a] != deg[b] ? deg[a] > deg[b] : tie[a] < tie[b]; });
     std::vector<int> fwd(n);
     for (int pos = 0; pos < n; ++pos) fwd[order[pos]] = pos;
     std::vector<int> inv(n);
     for (int v = 0; v < n; ++v) inv[fwd[v]] = j.inv_g.empty() ? v : j.inv_g[v];
     j.g = j.g.permuted(fwd);
     j.inv_g = std::move(inv);
+    if (seed) {
+        const int m = j.h.n;
+        const std::vector<int> ph = random_permutation(m, seed);
+        std::vector<int> ih(m);
+        for (int u = 0; u < m; ++u) ih[ph[u]] = j.inv_h.empty() ? u : j.inv_h[u];
+        j.h = j.h.permuted(ph);
+        j.inv_h = std::move(ih);
+    }
 }
 
 double secs_since(std::chrono::steady_clock::time_point t0) {
@@ -298,7 +316,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     f.n_groups = n_groups;
     const bool parity = o.mode == MCSG_MODE_PARITY;
     if (!parity && !ex.relabeled)
-        for (Job& j : jobs) relabel_for_throughput(j);
+        for (Job& j : jobs) relabel_for_throughput(j, j.seed ? j.seed : o.seed);
     plan(ctx, jobs, o, &f);
     const int n = f.n;
     ctx.reserve(size_t(n), size_t(n_groups), size_t(f.warps));
@@ -527,7 +545,7 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
     job.goal = o.goal;
     job.floor_size = o.floor_size;
     job.group = 0;
-    relabel_for_throughput(job);
+    relabel_for_throughput(job, o.seed);
     InstanceDesc desc;
     pack_instance(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, &desc);
     const int per_dev = o.frontier > 0 ? o.frontier : 256;
@@ -803,8 +821,8 @@ int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg
 }
 
 int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
-                       const int32_t* orders, const mcsg_options* opt, mcsg_result* out,
-                       int32_t* winner_out, mcsg_stats* stats) {
+                       const int32_t* orders, const uint64_t* seeds, const mcsg_options* opt,
+                       mcsg_result* out, int32_t* winner_out, mcsg_stats* stats) {
     try {
         const auto t0 = std::chrono::steady_clock::now();
         const mcsg_options o = defaults(opt);
@@ -818,6 +836,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
         std::vector<Job> jobs;
         for (int i = 0; i < count; ++i) {
             jobs.push_back(make_job(G, H, orders ? orders[i] : MCSG_ORDER_NONE));
+            jobs.back().seed = seeds ? seeds[i] : 0;
             jobs.back().group = 0;
             jobs.back().goal = o.goal;
             jobs.back().floor_size = o.floor_size;
@@ -844,7 +863,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
                 index[i % D].push_back(i);
             }
             for (int d = 0; d < D; ++d)
-                for (Job& j : plans[d].jobs) relabel_for_throughput(j);
+                for (Job& j : plans[d].jobs) relabel_for_throughput(j, j.seed ? j.seed : o.seed);
             std::vector<DevicePlan> used;
             std::vector<std::vector<int>> used_index;
             for (int d = 0; d < D; ++d)
