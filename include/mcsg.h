@@ -92,7 +92,18 @@ typedef struct mcsg_options {
     int32_t n_devices;
     int32_t devices[16];
     int32_t frontier;               /* subtrees per device, 0 = 256 */
+    /* Dead-end handling (DeadEndPolicy heuristics.hpp:30-38, run_engine's
+     * forecast-then-jump composition portfolio.cpp:136-155): with a jump mode
+     * set, the search stops once the nodes since the last improvement reach
+     * deadend_abs (or deadend_rel x the nodes at that improvement) and a bound
+     * jump (MCSG_JUMP_*) resumes from the incumbent. */
+    uint64_t deadend_abs;           /* 0 = off */
+    double deadend_rel;             /* 0 = off */
+    int32_t deadend_jump;           /* 0 none, 1 plus_one, 2 doubling */
 } mcsg_options;
+
+#define MCSG_JUMP_PLUS_ONE 1
+#define MCSG_JUMP_DOUBLING 2
 
 typedef struct mcsg_stats {
     uint64_t nodes;          /* stats.recursions: counted search nodes */
@@ -123,7 +134,11 @@ typedef struct mcsg_result {
     int32_t pairs[2 * MCSG_MAX_N]; /* (v in G, u in H) in ORIGINAL ids */
     uint64_t nodes;          /* nodes of this instance */
     double solve_s;          /* device time from launch to this instance's proof */
+    int32_t flags;           /* MCSG_RESULT_SUSPECT: stopped by the dead-end policy */
+    int32_t probes;          /* goal / jump probes run for this result */
 } mcsg_result;
+
+#define MCSG_RESULT_SUSPECT 1
 
 /* ---- solving ---------------------------------------------------------- */
 int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,

@@ -96,7 +96,8 @@ class _Options(C.Structure):
                 ("goal", C.c_int32), ("disable_pruning", C.c_int32), ("floor_size", C.c_int32),
                 ("device", C.c_int32), ("max_warps", C.c_int32), ("smem_classes", C.c_int32),
                 ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32)),
-                ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32)]
+                ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32),
+                ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -111,7 +112,8 @@ class _Stats(C.Structure):
 
 class _Result(C.Structure):
     _fields_ = [("status", C.c_int32), ("size", C.c_int32), ("pairs", C.c_int32 * (2 * MAX_N)),
-                ("nodes", C.c_uint64), ("solve_s", C.c_double)]
+                ("nodes", C.c_uint64), ("solve_s", C.c_double), ("flags", C.c_int32),
+                ("probes", C.c_int32)]
 
 
 _lib = None
@@ -373,11 +375,14 @@ class SolveConfig:
     seed: int = 0
     devices: tuple = ()                # > 1 entry: shard one instance over these GPUs
     frontier: int = 0                  # host-expanded subtrees per device (0 = 256)
+    deadend: tuple | None = None       # ("abs", n) | ("rel", mult): DeadEndPolicy
+    deadend_jump: "JumpMode | None" = None  # jump that resumes after a suspect verdict
 
 
 @dataclass
 class SearchStats:
     recursions: int = 0
+    deadend_suspects: int = 0
     wall_seconds: float = 0.0
     kernel_seconds: float = 0.0
     solve_seconds: float = 0.0
@@ -435,6 +440,16 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
     for i, dv in enumerate(cfg.devices):
         o.devices[i] = int(dv)
     o.frontier = cfg.frontier
+    if cfg.deadend is not None:
+        kind, val = cfg.deadend
+        if kind == "abs":
+            o.deadend_abs = int(val)
+        elif kind == "rel":
+            o.deadend_rel = float(val)
+        else:
+            raise GraphError(f"unknown deadend policy '{kind}'")
+        if cfg.deadend_jump is not None:
+            o.deadend_jump = 2 if cfg.deadend_jump == JumpMode.doubling else 1
     for k, v in over.items():
         setattr(o, k, v)
     return o
@@ -442,7 +457,8 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
 
 def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
     pairs = [(int(r.pairs[2 * i]), int(r.pairs[2 * i + 1])) for i in range(r.size)]
-    s = SearchStats(recursions=int(r.nodes), solve_seconds=r.solve_s, seed=seed)
+    s = SearchStats(recursions=int(r.nodes), solve_seconds=r.solve_s, seed=seed, probes=int(r.probes),
+                    deadend_suspects=int(r.flags & 1))
     if st is not None:
         s.wall_seconds = st.wall_s
         s.kernel_seconds = st.kernel_s
@@ -628,6 +644,12 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
         return solve_goal_directed(g, h, cfg)
     if spec.restart_seed is not None:
         return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, seed=spec.restart_seed))
+    if spec.deadend is not None:
+        # forecast-then-mitigate (portfolio.cpp:136-155): a monitored all-warp
+        # solve; with a jump configured, a suspect verdict hands the incumbent
+        # to the bound jump (without one the monitor never stops the search)
+        return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, deadend=spec.deadend,
+                                               deadend_jump=spec.jump))
     if spec.jump is not None:
         return bound_jump_search(g, h, 0, spec.jump, cfg)
     return solve(g, h, dataclasses.replace(cfg, mode=MODE_PARITY))

@@ -54,11 +54,16 @@ struct InstanceState {
 
 // Incumbent group (one per solved pair; several instances when a portfolio
 // races orderings/strategies on one GPU and shares the size).
-struct GroupState {
+struct alignas(16) GroupState {
     uint32_t best;          // monotone size, only raised after a mapping of that size is stored
-    uint32_t done;          // 1: max reached, goal reached, or one member proved optimality
+    uint32_t done;          // 1: max reached, goal reached, suspect, or one member proved optimality
     int32_t winner;         // instance that proved / reached first (-1 none)
     int32_t reached;        // goal probes: 1 when |M| >= goal was found
+    // dead-end monitor (heuristics.hpp:30-60), only when a policy is set
+    uint32_t suspect;       // 1: the policy fired and stopped the search
+    uint32_t pad;
+    unsigned long long nodes;       // nodes counted so far (per poll interval)
+    unsigned long long at_improve;  // `nodes` when the incumbent last improved
 };
 
 // A frozen subtree: the node's classes and mapping, the selected class and
@@ -147,6 +152,11 @@ struct KernelParams {
     int32_t donate;          // 0 = parity mode (no donation: exact sequential semantics)
     int32_t poll_interval;   // poll global state every poll_interval nodes
     Counters* counters;
+    // dead-end policy (DeadEndPolicy, heuristics.hpp:30-38; deadend_check,
+    // heuristics.cpp:103-112): suspect when nodes since the last improvement
+    // reach deadend_abs, or deadend_rel * max(1, nodes at the improvement)
+    unsigned long long deadend_abs;  // 0 = off
+    double deadend_rel;              // 0 = off
 };
 
 }  // namespace mcsg

@@ -166,12 +166,14 @@ struct JobResult {
     uint64_t nodes = 0;
     double solve_s = 0;
     bool completed = false;
+    bool suspect = false;  // the dead-end policy stopped it
 };
 
 struct GroupResult {
     bool done = false;
     int winner = -1;
     bool reached = false;
+    bool suspect = false;
 };
 
 struct LaunchOut {
@@ -381,6 +383,10 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.donate = parity ? 0 : 1;
     p.poll_interval = parity ? 4096 : 256;
     p.counters = ctx.d_cnt;
+    if (!parity && o.deadend_jump != 0) {  // the monitor only stops when a jump follows
+        p.deadend_abs = o.deadend_abs;
+        p.deadend_rel = o.deadend_rel;
+    }
 
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
     ck(kernel_launch(f.wide, f.directed, parity, p, f.ctas, ctx.stream), "search kernel launch");
@@ -430,6 +436,7 @@ LaunchOut finish(InFlight& f) {
         out.groups[gi].done = ctx.h_grp[gi].done != 0;
         out.groups[gi].winner = ctx.h_grp[gi].winner;
         out.groups[gi].reached = ctx.h_grp[gi].reached != 0;
+        out.groups[gi].suspect = ctx.h_grp[gi].suspect != 0;
     }
     for (int i = 0; i < n; ++i) {
         const InstanceState& s = ctx.h_ist[i];
@@ -440,8 +447,13 @@ LaunchOut finish(InFlight& f) {
         r.size = int(s.map_size);
         r.solve_s = s.t_done_ns > out.counters.t_start_ns ? (s.t_done_ns - out.counters.t_start_ns) * 1e-9 : 0.0;
         const bool group_done = out.groups[j.group].done;
+        // a suspect verdict abandons the remaining tasks (they still finish, so
+        // the open-task count says nothing about completion here)
+        r.suspect = out.groups[j.group].suspect;
         if (stop != 0 && !(r.completed || group_done))
             r.status = stop == 2 ? MCSG_CANCELLED : MCSG_TIMEOUT;
+        else if (r.suspect)
+            r.status = MCSG_TIMEOUT;  // stopped by the dead-end policy; the caller resumes (jump)
         else
             r.status = MCSG_OPTIMAL;
         r.pairs.resize(2 * r.size);
@@ -675,6 +687,7 @@ void write_result(const HostGraph& g, const HostGraph& h, const JobResult& r, mc
     out->size = r.size;
     out->nodes = r.nodes;
     out->solve_s = r.solve_s;
+    out->flags = r.suspect ? MCSG_RESULT_SUSPECT : 0;
     if (r.size > 0 && verify(g, h, r.pairs.data(), r.size) != 1)
         throw Error("internal error: kernel returned an invalid mapping");
     for (int k = 0; k < 2 * r.size; ++k) out->pairs[k] = r.pairs[k];
@@ -790,6 +803,38 @@ int32_t mcsg_solve_batch(int32_t count, const mcsg_graph* gs, const mcsg_graph* 
 int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
                    mcsg_result* out, mcsg_stats* stats) {
     const mcsg_options o = defaults(opt);
+    if (o.n_devices <= 1 && o.deadend_jump != 0 && (o.deadend_abs || o.deadend_rel > 0)) {
+        // forecast-then-mitigate (portfolio.cpp:136-155): monitored solve; on a
+        // suspect verdict the bound jump resumes from the incumbent size
+        const auto t0 = std::chrono::steady_clock::now();
+        const int32_t rc = mcsg_solve_batch(1, g, h, &o, out, stats);
+        if (rc == MCSG_ERROR || !(out->flags & MCSG_RESULT_SUSPECT)) return rc;
+        mcsg_options rest = o;
+        rest.deadend_jump = 0;
+        if (o.budget_s < 1e8) {
+            rest.budget_s = o.budget_s - secs_since(t0);
+            if (rest.budget_s <= 0) return out->status;
+        }
+        mcsg_result first = *out;
+        mcsg_stats st2{};
+        const int32_t rc2 = mcsg_bound_jump(g, h, first.size, o.deadend_jump == MCSG_JUMP_DOUBLING ? 1 : 0,
+                                            &rest, out, &st2);
+        if (rc2 == MCSG_ERROR) return rc2;
+        if (out->size < first.size) {  // keep the better witness
+            out->size = first.size;
+            std::memcpy(out->pairs, first.pairs, sizeof(first.pairs));
+        }
+        out->nodes += first.nodes;
+        out->flags = MCSG_RESULT_SUSPECT;
+        if (stats) {
+            stats->nodes += st2.nodes;
+            stats->probes = st2.probes;
+            stats->kernel_s += st2.kernel_s;
+            stats->launches += st2.launches;
+            stats->wall_s = secs_since(t0);
+        }
+        return out->status;
+    }
     if (o.n_devices <= 1) return mcsg_solve_batch(1, g, h, opt, out, stats);
     try {
         const auto t0 = std::chrono::steady_clock::now();
@@ -955,6 +1000,7 @@ int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
         write_result(G, H, r, out);
         if (stats) {
             stats->probes = probes;
+            out->probes = int32_t(probes);
             stats->wall_s = secs_since(t0);
         }
         return out->status;
@@ -1028,6 +1074,7 @@ int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t curren
         write_result(G, H, r, out);
         if (stats) {
             stats->probes = probes;
+            out->probes = int32_t(probes);
             stats->wall_s = secs_since(t0);
         }
         return out->status;

@@ -287,6 +287,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                     is->map_size = unsigned(dd + 1);
                     __threadfence();
                     atomicMax(&gs->best, unsigned(dd + 1));
+                    // DeadEndMonitor::note_improvement (heuristics.hpp:45)
+                    if (p.deadend_abs || p.deadend_rel > 0.0)
+                        atomicMax(&gs->at_improve, *reinterpret_cast<volatile unsigned long long*>(&gs->nodes));
                 }
                 // push the size to the other devices' incumbents (NVLink P2P)
                 if (grp == 0 && lane < p.n_peers) atomicMax_system(&p.peer_grp[lane]->best, unsigned(dd + 1));
@@ -334,6 +337,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             if (PAR) return true;
             if (gd != 0) return false;
             if (gb > best_eff) raise_best(gb);
+            if (p.deadend_abs || p.deadend_rel > 0.0) {
+                // deadend_check (heuristics.cpp:103-112) over the group's node count
+                int sus = 0;
+                if (lane == 0) {
+                    const unsigned long long total =
+                        atomicAdd(&gs->nodes, (unsigned long long)interval) + (unsigned long long)interval;
+                    const unsigned long long at = *reinterpret_cast<volatile unsigned long long*>(&gs->at_improve);
+                    const unsigned long long since = total - at;
+                    sus = (p.deadend_abs && since >= p.deadend_abs) ||
+                          (p.deadend_rel > 0.0 && double(since) >= p.deadend_rel * double(at > 0 ? at : 1ull));
+                    if (sus) {
+                        gs->suspect = 1u;
+                        atomicExch(&gs->done, 1u);
+                    }
+                }
+                if (__shfl_sync(kFull, sus, 0)) return false;
+            }
             if (waiting <= 0 || d <= root) return true;
             // donate the shallowest level that still owns work
             int f = -1;
