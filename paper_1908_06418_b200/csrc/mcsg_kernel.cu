@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             __syncwarp();
             if (lane == 0) st_release(&slot->seq, slot_pos + p.cap_mask + 1);  // free the slot
             x.load_level(0, nc);
-            x.prep_v(v);
+            x.prep_v(v, sel);
             at_next = true;
             // task-level prune (engine_parallel.cpp:148-155): every child would prune
             if (bound <= prn_thr) skip = true;
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 else v = Bits<W>::ctz(lsel);  // G is relabelled in select_vertex order
                 cand = x.class_r(sel);
             }
-            x.prep_v(v);
+            x.prep_v(v, sel);
             cont = 1;
 
         next:
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 cont = fr_cont(f);
             }
             x.load_level(base, nc);
-            x.prep_v(v);
+            x.prep_v(v, sel);
             goto next;
         }
 #undef MCSG_COUNT_NODE

@@ -179,6 +179,7 @@ struct Search {
     W L[S], R[S];
     W LX[S];        // L with the branching vertex v removed
     int lc[S][P];   // |LX ∩ part_q(v)|
+    int rs[S];      // |R| minus 1 on the selected class (u leaves exactly that class)
     bool two = false;  // 64-bit kernel: the level has classes in the second slot (nc > 32)
 
     // slot k holds live classes (slot 0 always; slot 1 only when nc > 32)
@@ -287,7 +288,7 @@ struct Search {
     }
 
     // After choosing v: LX = L \ {v}, and the per-part left counts.
-    __device__ __forceinline__ void prep_v(int v) {
+    __device__ __forceinline__ void prep_v(int v, int sel) {
         W g[P];
         g_parts(v, g);
         const W vb = W(1) << v;
@@ -297,8 +298,10 @@ struct Search {
             if (!live(k)) {
 #pragma unroll
                 for (int q = 0; q < P; ++q) lc[k][q] = 0;
+                rs[k] = 0;
                 continue;
             }
+            rs[k] = Bits<W>::popc(R[k]) - (lane + 32 * k == sel ? 1 : 0);
             if constexpr (!DIR) {
                 const int a = Bits<W>::popc(LX[k] & g[1]);
                 lc[k][1] = a;
@@ -311,20 +314,27 @@ struct Search {
     }
 
     // Bound of the child (v,u) minus |M|+1: Σ_c Σ_parts min(|L_part|, |R_part|).
+    // u is in no adjacency row of its own, so it only ever sits in part 0 of
+    // the selected class: |R\{u} ∩ part_q| = |R ∩ part_q| for q > 0, and part
+    // 0 follows from rs = |R| - [selected] by subtraction (no per-u masking).
     __device__ __forceinline__ unsigned child_sum(int u, const W h[P]) const {
-        const W ub = W(1) << u;
+        (void)u;
         unsigned sm = 0;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
             if (!live(k)) continue;
-            const W rx = R[k] & ~ub;
             if constexpr (!DIR) {
-                const int b = Bits<W>::popc(rx & h[1]);
-                const int r0 = Bits<W>::popc(rx) - b;
-                sm += unsigned(min(lc[k][0], r0) + min(lc[k][1], b));
+                const int b = Bits<W>::popc(R[k] & h[1]);
+                sm += unsigned(min(lc[k][0], rs[k] - b) + min(lc[k][1], b));
             } else {
+                int rest = rs[k];
 #pragma unroll
-                for (int q = 0; q < P; ++q) sm += unsigned(min(lc[k][q], Bits<W>::popc(rx & h[q])));
+                for (int q = 1; q < P; ++q) {
+                    const int b = Bits<W>::popc(R[k] & h[q]);
+                    rest -= b;
+                    sm += unsigned(min(lc[k][q], b));
+                }
+                sm += unsigned(min(lc[k][0], rest));
             }
         }
         return __reduce_add_sync(kFull, sm);
