@@ -198,11 +198,21 @@ def run_ours(args, rank, world, local_rank):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the solver has no CPU path)")
-    torch.cuda.set_device(local_rank)
+    ndev = torch.cuda.device_count()
+    device = local_rank % ndev  # more ranks than GPUs only in CI-style dry runs
+    torch.cuda.set_device(device)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # No data-path collective: only barriers and the max/sum of timings.
+        # NCCL when every rank owns a GPU; gloo when ranks share one (NCCL
+        # refuses two ranks on the same device).
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group("gloo")
+
+    red_dev = "cuda" if (dist is not None and dist.get_backend() == "nccl") else "cpu"
 
     def barrier():
         if dist is not None:
@@ -212,14 +222,14 @@ def run_ours(args, rank, world, local_rank):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -228,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
     for i in idx:
         n, p, sg, sh = c2_pair_seeds(i)
         pairs.append((M.random_graph(n, p, sg), M.random_graph(n, p, sh)))
-    cfg = M.SolveConfig(mode=M.MODE_THROUGHPUT, device=local_rank)
+    cfg = M.SolveConfig(mode=M.MODE_THROUGHPUT, device=device)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
