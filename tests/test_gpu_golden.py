@@ -84,3 +84,23 @@ def test_c4_hard_pair_two_independent_modes():
     jr = M.bound_jump_search(g, h, r.size, M.JumpMode.plus_one,
                              M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=300))
     assert jr.status == M.SolveStatus.optimal and jr.size == r.size and M.verify(g, h, jr.best)
+
+
+def test_batch_mixed_statuses_under_budget():
+    """A budget that proves the easy pairs but not C4: per-instance statuses,
+    every returned mapping still verifies (solve.cpp:118-126 semantics)."""
+    gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))["sizes"]
+    pairs = c2_pairs()[:6]
+    c4 = (M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001))
+    res, _ = M.solve_batch(pairs + [c4], M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=1.0))
+    # warps are shared by every instance of the batch, so which small pairs
+    # finish inside the budget depends on scheduling; each status must be
+    # truthful: optimal => the reference optimum, timeout => a valid incumbent
+    for i, ((g, h), r) in enumerate(zip(pairs, res[:6])):
+        assert M.verify(g, h, r.best)
+        if r.status == M.SolveStatus.optimal:
+            assert r.size == gold[str(i)]
+        else:
+            assert r.status == M.SolveStatus.timeout and r.size <= gold[str(i)]
+    assert res[6].status == M.SolveStatus.timeout
+    assert 0 < res[6].size <= 16 and M.verify(*c4, res[6].best)
