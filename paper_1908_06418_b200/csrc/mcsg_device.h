@@ -45,7 +45,7 @@ struct InstanceState {
     uint32_t map_size;      // size of the mapping stored in map_v/map_u
     int32_t lock;           // spin lock guarding map_* on improvement
     int32_t open_tasks;     // tasks of this instance not yet finished
-    int32_t status;         // 0 running/optimal, 1 timeout/cancel-interrupted
+    int32_t workers;        // warps currently running a task of this instance (fairness)
     unsigned long long nodes;
     unsigned long long t_done_ns;  // %globaltimer when the last task finished
     uint8_t map_v[kMaxN];
@@ -125,6 +125,7 @@ struct Ctl {
     Line32 idle;       // warps waiting for work (donation trigger)
     Line32 stop;       // 0 run, 1 timeout, 2 cancelled, 3 internal error
     Line32 next_root;  // root tasks are implicit: instance ids handed out by atomicAdd
+    Line32 live;       // instances with unfinished tasks (fairness share)
 };
 
 constexpr int kMaxPeers = 16;

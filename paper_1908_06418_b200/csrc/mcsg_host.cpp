@@ -348,6 +348,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     *ctx.h_ctl = Ctl{};
     ctx.h_ctl->pending.v = (ex.roots ? n : 0) + int(ex.seeded.size());
     ctx.h_ctl->tail.v = ex.seeded.size();
+    ctx.h_ctl->live.v = n;
     ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
     if (!ex.seeded.empty()) {

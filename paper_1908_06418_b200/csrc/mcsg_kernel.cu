@@ -29,6 +29,12 @@
 
 namespace mcsg {
 
+// Fairness between the instances of one launch: an instance running on fewer
+// than half its share of the warps (warps / live instances) keeps donating
+// while fewer than kStarvedQueue subtrees are queued, even when no warp is
+// waiting; warps that finish a task take queued subtrees in ticket order.
+constexpr int kStarvedQueue = 256;
+
 template <typename W, bool DIR, bool PAR>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
     mcs_search_kernel(KernelParams p) {
@@ -169,6 +175,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
         InstanceState* const is = p.ist + inst;
         if (lane == 0) {
             s.st_tasks += 1;
+            if (!PAR) atomicAdd(&is->workers, 1);
             s.polled = 0;
         }
 
@@ -194,6 +201,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             if (!PAR && lane == 1) cp_async16(&s.pf[4], &ctl->head);
             if (!PAR && lane == 2) cp_async16(&s.pf[8], &ctl->tail);
             if (!PAR && lane == 3) cp_async16(&s.pf[12], gs);
+            if (!PAR && lane == 4) cp_async16(&s.pf[16], is);
+            if (!PAR && lane == 5) cp_async16(&s.pf[20], &ctl->live);
             cp_async_commit();
         };
         cp_async_wait_all();  // the previous task's copies must not land after these
@@ -354,7 +363,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 }
                 if (__shfl_sync(kFull, sus, 0)) return false;
             }
-            if (waiting <= 0 || d <= root) return true;
+            // Donate when warps wait for work, or — fairness between the
+            // instances of a batch — when this instance runs on few warps and
+            // the queue is short: a busy batch would otherwise never hand a
+            // small instance's subtrees to anyone (FIFO tickets serve them next).
+            const int workers = int(s.pf[19]);
+            const int live = max(int(s.pf[20]), 1);
+            const int total_warps = int(gridDim.x) * kWarpsPerCta;
+            const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
+            if ((waiting <= 0 && !starved) || d <= root) return true;
             // donate the shallowest level that still owns work
             int f = -1;
             for (int b0 = root; b0 < d && f < 0; b0 += 32) {
@@ -597,9 +614,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             s.st_splits += splits;
             if (task_nodes) atomicAdd(&is->nodes, task_nodes);
             if (!abort_all) {
+                if (!PAR) atomicSub(&is->workers, 1);
                 const int left = atomicSub(&is->open_tasks, 1) - 1;
                 if (left == 0) {
                     is->t_done_ns = globaltimer();
+                    atomicSub(&ctl->live.v, 1);
                     if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
                     // portfolio across devices: a complete member search proves
                     // the optimum for every member (portfolio.cpp:271-279)

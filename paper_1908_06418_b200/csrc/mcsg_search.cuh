@@ -139,8 +139,10 @@ struct WarpSmem {
     W in_h[DIR ? NB : 1];
     unsigned long long f_word[kMaxDepth + 1];
     // Control words prefetched one poll ahead with cp.async (16 B each):
-    // [0..3] the stop line, [4..7] ring head, [8..11] ring tail, [12..15] GroupState.
-    alignas(16) uint32_t pf[16];
+    // [0..3] the stop line, [4..7] ring head, [8..11] ring tail, [12..15] GroupState,
+    // [16..19] the first 16 B of the task's InstanceState (workers at [19]),
+    // [20..23] the live-instance line.
+    alignas(16) uint32_t pf[24];
     // per-warp counters kept out of registers (written by lane 0)
     unsigned long long polled;     // nodes of the current task counted at earlier polls
     unsigned long long st_nodes, st_splits, st_donations, st_tasks, st_spills;

@@ -93,14 +93,12 @@ def test_batch_mixed_statuses_under_budget():
     pairs = c2_pairs()[:6]
     c4 = (M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001))
     res, _ = M.solve_batch(pairs + [c4], M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=1.0))
-    # warps are shared by every instance of the batch, so which small pairs
-    # finish inside the budget depends on scheduling; each status must be
-    # truthful: optimal => the reference optimum, timeout => a valid incumbent
+    # the small pairs share the warps with C4; the kernel's fairness rule
+    # (instances below half their share of warps keep donating) proves them
+    # well inside the budget
     for i, ((g, h), r) in enumerate(zip(pairs, res[:6])):
         assert M.verify(g, h, r.best)
-        if r.status == M.SolveStatus.optimal:
-            assert r.size == gold[str(i)]
-        else:
-            assert r.status == M.SolveStatus.timeout and r.size <= gold[str(i)]
+        assert r.status == M.SolveStatus.optimal and r.size == gold[str(i)]
+        assert r.stats.solve_seconds < 1.0
     assert res[6].status == M.SolveStatus.timeout
     assert 0 < res[6].size <= 16 and M.verify(*c4, res[6].best)
