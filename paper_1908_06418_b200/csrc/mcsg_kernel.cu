@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 h.pad1 = 0;
                 sl->hdr = h;
                 s.f_cand[f] = keep;
-                s.f_word[f] = fw & ~(1ull << 41);  // the continuation left with the task
+                s.f_word[f] = fw & ~kFrameCont;  // the continuation left with the task
             }
             fence_acq_rel_gpu();  // payload before the release of the slot
             __syncwarp();

@@ -114,20 +114,23 @@ __device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
 // Packed DFS frame (one per search level): where the level's classes are,
 // which class/vertex it branches on, its bound, whether the v-unmatched
 // continuation is still owned, and the u of the child being explored.
+// Byte-aligned fields: packing is a chain of IMADs, unpacking byte extracts.
+//   low word : base (16 bits) | nc << 16 | sel << 24
+//   high word: v | bound << 8 | cont << 16 | u << 24
+constexpr unsigned long long kFrameCont = 1ull << 48;
 __device__ __forceinline__ unsigned long long pack_frame(int base, int nc, int sel, int v, int bound,
                                                          int cont, int u) {
-    return (unsigned long long)base | ((unsigned long long)nc << 14) |
-           ((unsigned long long)sel << 21) | ((unsigned long long)v << 28) |
-           ((unsigned long long)bound << 34) | ((unsigned long long)cont << 41) |
-           ((unsigned long long)u << 42);
+    const unsigned lo = unsigned(base) + (unsigned(nc) << 16) + (unsigned(sel) << 24);
+    const unsigned hi = unsigned(v) + (unsigned(bound) << 8) + (unsigned(cont) << 16) + (unsigned(u) << 24);
+    return (unsigned long long)lo | ((unsigned long long)hi << 32);
 }
-__device__ __forceinline__ int fr_base(unsigned long long f) { return int(f & 0x3fff); }
-__device__ __forceinline__ int fr_nc(unsigned long long f) { return int((f >> 14) & 0x7f); }
-__device__ __forceinline__ int fr_sel(unsigned long long f) { return int((f >> 21) & 0x7f); }
-__device__ __forceinline__ int fr_v(unsigned long long f) { return int((f >> 28) & 0x3f); }
-__device__ __forceinline__ int fr_bound(unsigned long long f) { return int((f >> 34) & 0x7f); }
-__device__ __forceinline__ int fr_cont(unsigned long long f) { return int((f >> 41) & 1); }
-__device__ __forceinline__ int fr_u(unsigned long long f) { return int((f >> 42) & 0x3f); }
+__device__ __forceinline__ int fr_base(unsigned long long f) { return int(unsigned(f) & 0xffffu); }
+__device__ __forceinline__ int fr_nc(unsigned long long f) { return int(__byte_perm(unsigned(f), 0, 0x4442)); }
+__device__ __forceinline__ int fr_sel(unsigned long long f) { return int(unsigned(f) >> 24); }
+__device__ __forceinline__ int fr_v(unsigned long long f) { return int(unsigned(f >> 32) & 0xffu); }
+__device__ __forceinline__ int fr_bound(unsigned long long f) { return int(__byte_perm(unsigned(f >> 32), 0, 0x4441)); }
+__device__ __forceinline__ int fr_cont(unsigned long long f) { return int(__byte_perm(unsigned(f >> 32), 0, 0x4442)); }
+__device__ __forceinline__ int fr_u(unsigned long long f) { return int(unsigned(f >> 32) >> 24); }
 
 // Per-warp shared-memory image; the class stack follows it.
 template <typename W, bool DIR>
