@@ -21,6 +21,7 @@
  *   mcsg_load_graph_file       mcs::load_graph_file                       graph_io.hpp:33
  *   mcsg_save_graph_file       mcs::save_graph_file                       graph_io.hpp:34
  *   mcsg_pack_graph            (the loader's bitset packing; no reference counterpart)
+ *   mcsg_pack_graph_words      (the same, multi-word rows for 64 < n <= 255)
  *
  * Graphs use the reference's storage: an n*n row-major byte matrix of
  * adjacency codes (graph.hpp:40,60): 0 none; undirected 1 = edge; directed
@@ -40,7 +41,7 @@
 extern "C" {
 #endif
 
-#define MCSG_ABI_VERSION 1
+#define MCSG_ABI_VERSION 2
 
 /* status codes (mirror mcs_main.cpp:22-24 exit codes; SolveStatus solve.hpp:23) */
 #define MCSG_OPTIMAL 0
@@ -62,7 +63,7 @@ extern "C" {
 #define MCSG_ORDER_COMPONENTS 2
 #define MCSG_ORDER_BLOCK 3
 
-#define MCSG_MAX_N 64
+#define MCSG_MAX_N 255
 
 typedef struct mcsg_graph {
     int32_t n;
@@ -179,6 +180,9 @@ int32_t mcsg_save_graph_file(const mcsg_graph* g, const char* path, int32_t form
  * undirected adjacency / directed forward bits; in_rows[n] (may be NULL)
  * the directed backward bits. */
 int32_t mcsg_pack_graph(const mcsg_graph* g, uint64_t* out_rows, uint64_t* in_rows);
+/* The same for any n <= MCSG_MAX_N: row v is words[v*words .. v*words+words),
+ * bit x%64 of word x/64 (the wide kernels' form). words >= ceil(n/64). */
+int32_t mcsg_pack_graph_words(const mcsg_graph* g, int32_t words, uint64_t* out_rows, uint64_t* in_rows);
 
 /* ---- runtime ------------------------------------------------------------ */
 const char* mcsg_last_error(void);

@@ -41,7 +41,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmcsg.so")
-MAX_N = 64
+MAX_N = 255
 
 __all__ = [
     "Graph", "GraphError", "ParseError", "from_edge_list", "random_graph", "random_permutation",
@@ -144,6 +144,7 @@ def lib():
                                            P(C.c_uint8), P(C.c_int32)]
         L.mcsg_save_graph_file.argtypes = [G, C.c_char_p, C.c_int32]
         L.mcsg_pack_graph.argtypes = [G, P(C.c_uint64), P(C.c_uint64)]
+        L.mcsg_pack_graph_words.argtypes = [G, C.c_int32, P(C.c_uint64), P(C.c_uint64)]
         L.mcsg_last_error.restype = C.c_char_p
         L.mcsg_last_error_kind.restype = C.c_int32
         L.mcsg_abi_version.restype = C.c_int32
@@ -338,6 +339,18 @@ def pack_graph(g: Graph):
     inn = np.zeros(max(g.n(), 1), np.uint64)
     if lib().mcsg_pack_graph(C.byref(g._c()), out.ctypes.data_as(C.POINTER(C.c_uint64)),
                              inn.ctypes.data_as(C.POINTER(C.c_uint64))) != 0:
+        raise _err()
+    return out[: g.n()].copy(), inn[: g.n()].copy()
+
+
+def pack_graph_words(g: Graph, words: int | None = None):
+    """Multi-word device rows (n <= 255): arrays of shape (n, words), bit x%64
+    of word x//64 (the wide kernels' form)."""
+    w = words if words is not None else max(1, (g.n() + 63) // 64)
+    out = np.zeros((max(g.n(), 1), w), np.uint64)
+    inn = np.zeros((max(g.n(), 1), w), np.uint64)
+    if lib().mcsg_pack_graph_words(C.byref(g._c()), w, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                   inn.ctypes.data_as(C.POINTER(C.c_uint64))) != 0:
         raise _err()
     return out[: g.n()].copy(), inn[: g.n()].copy()
 

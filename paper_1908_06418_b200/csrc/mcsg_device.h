@@ -19,6 +19,12 @@ namespace mcsg {
 constexpr int kMaxN = 64;        // one 64-bit word per bitset row (all configs n <= 45)
 constexpr int kMaxDepth = kMaxN + 1;
 constexpr int kWarpsPerCta = 4;
+// Wide graphs (64 < n <= 255): bitset rows of kWideWords 64-bit words. Vertex
+// ids, class counts and bounds still fit one byte (the frame/mapping layout of
+// the 64-bit kernel), like the reference's byte-frame engine (K254 accepted,
+// K255 rejected: engine_iterative.hpp:9, test_engine_iterative.cpp:40-59).
+constexpr int kMaxWideN = 255;
+constexpr int kWideWords = 4;
 
 // Per-instance read-only description, packed by the host loader
 // (graph.hpp:31-62 codes -> bitsets). 64-bit storage even when the kernel
@@ -48,8 +54,27 @@ struct InstanceState {
     int32_t workers;        // warps currently running a task of this instance (fairness)
     unsigned long long nodes;
     unsigned long long t_done_ns;  // %globaltimer when the last task finished
-    uint8_t map_v[kMaxN];
-    uint8_t map_u[kMaxN];
+    uint8_t map_v[kMaxWideN + 1];
+    uint8_t map_u[kMaxWideN + 1];
+};
+
+// Wide instance description (n <= 255): same header fields as InstanceDesc,
+// rows of kWideWords words (the 128-vertex kernel reads the first two).
+struct WideDesc {
+    int32_t n_g, n_h;
+    int32_t maxp;
+    int32_t goal;
+    int32_t n_init;
+    int32_t group;
+    int32_t prune;
+    int32_t floor;
+    uint64_t out_g[kMaxWideN + 1][kWideWords];
+    uint64_t out_h[kMaxWideN + 1][kWideWords];
+    uint64_t in_g[kMaxWideN + 1][kWideWords];
+    uint64_t in_h[kMaxWideN + 1][kWideWords];
+    uint64_t init_l[kMaxWideN + 1][kWideWords];
+    uint64_t init_r[kMaxWideN + 1][kWideWords];
+    uint32_t vkey[kMaxWideN + 1];  // (1023 - deg) << 8 | id  (degree <= 2 * 254 when directed)
 };
 
 // Incumbent group (one per solved pair; several instances when a portfolio
@@ -95,6 +120,18 @@ struct alignas(128) TaskSlot {
     uint64_t cls_r[kMaxN];
 };
 
+// Wide frozen subtree (n <= 255): the remaining u set and the classes are
+// kWideWords words per bitset; hdr.cand is unused.
+struct alignas(128) WideSlot {
+    unsigned long long seq;
+    unsigned long long pad[1];
+    TaskHeader hdr;
+    uint64_t cand[kWideWords];
+    uint8_t map_v[kMaxWideN + 1];
+    uint8_t map_u[kMaxWideN + 1];
+    uint64_t cls[kMaxWideN][2][kWideWords];  // [class][L, R][word]
+};
+
 // Global counters (one set per launch), for the roofline / stats.
 struct Counters {
     unsigned long long nodes;
@@ -131,10 +168,12 @@ struct Ctl {
 constexpr int kMaxPeers = 16;
 
 struct KernelParams {
-    const InstanceDesc* inst;
+    const InstanceDesc* inst;   // n <= 64 kernels
+    const WideDesc* winst;      // wide kernels
     InstanceState* ist;
     GroupState* grp;
-    TaskSlot* slots;
+    TaskSlot* slots;            // n <= 64 kernels
+    WideSlot* wslots;           // wide kernels
     Ctl* ctl;
     uint32_t cap_mask;       // ring capacity - 1 (power of two)
     int32_t n_inst;
@@ -147,7 +186,7 @@ struct KernelParams {
     int32_t peer_done_on_complete;  // portfolio: the first device to finish proves for all
     const volatile int32_t* cancel;  // host-mapped cancel flag (may be null)
     unsigned long long budget_ns;    // per-warp deadline = warp start + budget, 0 = none
-    uint64_t* spill;         // per-warp HBM spill area for class levels (64-bit kernel only)
+    uint64_t* spill;         // per-warp HBM spill area for class levels (64-bit and wide kernels)
     int32_t spill_classes;   // classes per warp in the spill area
     int32_t smem_classes;    // classes per warp in shared memory
     int32_t donate;          // 0 = parity mode (no donation: exact sequential semantics)

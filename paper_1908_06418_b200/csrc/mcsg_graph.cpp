@@ -445,4 +445,61 @@ void pack_instance(const HostGraph& g, const HostGraph& h, int goal, bool prune,
     d->n_init = nc;
 }
 
+// The same device form for 64 < n <= 255: rows of kWideWords words (bit x%64
+// of word x/64), vertex key (1023 - degree) << 8 | id (a directed degree
+// reaches 2 * 254).
+void pack_wide(const HostGraph& g, const HostGraph& h, int goal, bool prune, int floor_size, int group,
+               WideDesc* d) {
+    if (g.directed != h.directed) throw Error("solve: graphs must share a kind");
+    if (g.labeled != h.labeled) throw Error("cannot mix a labeled graph with an unlabeled one");
+    if (g.n > kMaxWideN || h.n > kMaxWideN)
+        throw Error("graphs above " + std::to_string(kMaxWideN) + " vertices are not supported (n=" +
+                    std::to_string(std::max(g.n, h.n)) + ")");
+    std::memset(d, 0, sizeof(*d));
+    d->n_g = g.n;
+    d->n_h = h.n;
+    d->maxp = std::min(g.n, h.n);
+    d->goal = goal;
+    d->prune = prune ? 1 : 0;
+    d->floor = floor_size;
+    d->group = group;
+    auto set = [](uint64_t* row, int x) { row[x >> 6] |= 1ull << (x & 63); };
+    auto rows = [&](const HostGraph& x, uint64_t (*out)[kWideWords], uint64_t (*in)[kWideWords]) {
+        for (int v = 0; v < x.n; ++v)
+            for (int u = 0; u < x.n; ++u) {
+                const uint8_t c = x.code(v, u);
+                if (c & 1u) set(out[v], u);
+                if (c & 2u) set(in[v], u);
+            }
+    };
+    rows(g, d->out_g, d->in_g);
+    rows(h, d->out_h, d->in_h);
+    for (int v = 0; v <= kMaxWideN; ++v) d->vkey[v] = 0xffffffffu;
+    for (int v = 0; v < g.n; ++v) d->vkey[v] = uint32_t(((1023 - g.degree(v)) << 8) | v);
+    int nc = 0;
+    if (!g.labeled) {
+        if (g.n > 0 && h.n > 0) {
+            for (int v = 0; v < g.n; ++v) set(d->init_l[0], v);
+            for (int u = 0; u < h.n; ++u) set(d->init_r[0], u);
+            nc = 1;
+        }
+    } else {
+        std::vector<int32_t> labs(g.labels.begin(), g.labels.end());
+        std::sort(labs.begin(), labs.end());
+        labs.erase(std::unique(labs.begin(), labs.end()), labs.end());
+        for (int32_t lab : labs) {
+            bool l = false, r = false;
+            for (int v = 0; v < g.n; ++v) l |= g.labels[v] == lab;
+            for (int u = 0; u < h.n; ++u) r |= h.labels[u] == lab;
+            if (!(l && r)) continue;
+            for (int v = 0; v < g.n; ++v)
+                if (g.labels[v] == lab) set(d->init_l[nc], v);
+            for (int u = 0; u < h.n; ++u)
+                if (h.labels[u] == lab) set(d->init_r[nc], u);
+            ++nc;
+        }
+    }
+    d->n_init = nc;
+}
+
 }  // namespace mcsg

@@ -47,5 +47,7 @@ void save_graph_file(const HostGraph& g, const std::string& path, int format);
 
 void pack_instance(const HostGraph& g, const HostGraph& h, int goal, bool prune, int floor_size,
                    int group, InstanceDesc* d);
+void pack_wide(const HostGraph& g, const HostGraph& h, int goal, bool prune, int floor_size, int group,
+               WideDesc* d);
 
 }  // namespace mcsg

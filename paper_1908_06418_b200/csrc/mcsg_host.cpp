@@ -26,11 +26,14 @@
 
 namespace mcsg {
 
-int kernel_occupancy(bool wide, bool directed, int smem_classes);
-int kernel_smem_per_warp(bool wide, bool directed, int smem_classes);
-cudaError_t kernel_launch(bool wide, bool directed, bool parity, const KernelParams& p, int ctas,
-                          cudaStream_t st);
+// kernel flavours by bitset width (mcsg_kernel.cu): 32, 64, 128, 256
+int kernel_occupancy(int bits, bool directed, int smem_classes);
+int kernel_smem_per_warp(int bits, bool directed, int smem_classes);
+int kernel_smem_fixed(int bits, bool directed);
+int kernel_class_bytes(int bits);
+cudaError_t kernel_launch(int bits, bool directed, bool parity, const KernelParams& p, int ctas, cudaStream_t st);
 cudaError_t ring_reset(TaskSlot* slots, uint32_t cap, Counters* c, cudaStream_t st);
+cudaError_t ring_reset_wide(WideSlot* slots, uint32_t cap, Counters* c, cudaStream_t st);
 
 namespace {
 
@@ -46,7 +49,13 @@ void ck(cudaError_t e, const char* what) {
 }
 
 constexpr uint32_t kRingCap = 16384;                      // power of two
-constexpr int kSpillClasses = kMaxDepth * kMaxN;          // worst-case stack: no overflow possible
+constexpr uint32_t kWideRingCap = 4096;                   // wide slots are 17 KB
+constexpr int kSpillClasses = kMaxDepth * kMaxN;          // 64-bit kernel: worst-case stack, no overflow possible
+
+// Bitset width of the kernel flavour that fits n vertices.
+int bits_for(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+// Vertex capacity of a flavour (the wide 256-bit flavour stops at 255).
+int capacity_of(int bits) { return bits == 256 ? kMaxWideN : bits; }
 
 struct Context {
     int device = 0;
@@ -55,6 +64,10 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     InstanceDesc* d_inst = nullptr;
+    WideDesc* d_winst = nullptr;    // wide instances (n > 64), allocated on first use
+    WideDesc* h_winst = nullptr;
+    size_t winst_cap = 0;
+    WideSlot* d_wslots = nullptr;   // wide ring, allocated on first use
     InstanceState* d_ist = nullptr;
     GroupState* d_grp = nullptr;
     InstanceDesc* h_inst = nullptr;
@@ -67,7 +80,7 @@ struct Context {
     Counters* h_cnt = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     uint64_t* d_spill = nullptr;
-    size_t spill_warps = 0;
+    size_t spill_bytes = 0;
     int32_t* h_cancel = nullptr;  // pinned, mapped
     int32_t* d_cancel = nullptr;
     std::mutex mu;
@@ -94,7 +107,7 @@ struct Context {
         *h_cancel = 0;
     }
 
-    void reserve(size_t n_inst, size_t n_grp, size_t warps) {
+    void reserve(size_t n_inst, size_t n_grp, size_t spill) {
         if (n_inst > inst_cap) {
             size_t cap = std::max<size_t>(n_inst, inst_cap * 2);
             cudaFree(d_inst);
@@ -115,10 +128,25 @@ struct Context {
             ck(cudaMallocHost(&h_grp, sizeof(GroupState) * cap), "groups host");
             grp_cap = cap;
         }
-        if (warps > spill_warps) {
+        if (spill > spill_bytes) {
             cudaFree(d_spill);
-            ck(cudaMalloc(&d_spill, sizeof(uint64_t) * 2 * kSpillClasses * warps), "spill");
-            spill_warps = warps;
+            d_spill = nullptr;
+            ck(cudaMalloc(&d_spill, spill), "spill");
+            spill_bytes = spill;
+        }
+    }
+
+    void reserve_wide(size_t n_inst) {
+        if (!d_wslots) {
+            ck(cudaMalloc(&d_wslots, sizeof(WideSlot) * kWideRingCap), "wide ring");
+        }
+        if (n_inst > winst_cap) {
+            size_t cap = std::max<size_t>(n_inst, winst_cap * 2);
+            cudaFree(d_winst);
+            cudaFreeHost(h_winst);
+            ck(cudaMalloc(&d_winst, sizeof(WideDesc) * cap), "wide instances");
+            ck(cudaMallocHost(&h_winst, sizeof(WideDesc) * cap), "wide instances host");
+            winst_cap = cap;
         }
     }
 };
@@ -260,7 +288,10 @@ struct InFlight {
     std::vector<Job>* jobs = nullptr;
     mcsg_options o{};
     int n = 0, n_groups = 0, ctas = 0, warps = 0, smem_classes = 0;
-    bool wide = false, directed = false;
+    int bits = 32;          // kernel flavour (bitset width)
+    bool directed = false;
+    int spill_classes = 0;  // per warp, in HBM
+    size_t spill_bytes = 0;
     size_t seeded = 0;
     std::chrono::steady_clock::time_point t_stage;
     double h2d_s = 0;
@@ -268,35 +299,39 @@ struct InFlight {
 
 // Kernel shape for a batch: specialisation, shared-memory class stack, grid.
 void plan(Context& ctx, const std::vector<Job>& jobs, const mcsg_options& o, InFlight* f) {
-    f->wide = false;
+    int maxn = 0, maxm = 0;
     f->directed = false;
     for (const Job& j : jobs) {
-        f->wide |= std::max(j.g.n, j.h.n) > 32;
+        maxn = std::max(maxn, std::max(j.g.n, j.h.n));
+        maxm = std::max(maxm, std::min(j.g.n, j.h.n));
         f->directed |= j.g.directed;
     }
+    f->bits = bits_for(maxn);
     const bool parity = o.mode == MCSG_MODE_PARITY;
     // Shared-memory class stack. A search level at depth d holds at most
-    // min(n_G, n_H) - d classes, so m(m+1)/2 (+ one level of slack) bounds the
-    // whole path: the 32-bit kernel never spills. The 64-bit kernel takes
-    // what the register-limited occupancy leaves and spills beyond it.
-    int maxm = 0;
-    for (const Job& j : jobs) maxm = std::max(maxm, std::min(j.g.n, j.h.n));
-    const int path_bound = maxm * (maxm + 1) / 2 + 2 * kMaxN;
+    // min(n_G, n_H) - d classes, so m(m+1)/2 (+ slack for one child's worst
+    // case) bounds the whole path: the 32-bit kernel never spills. The other
+    // flavours take what the register-limited occupancy leaves and spill
+    // whole levels beyond it to HBM. Level 0 (a root or a donated subtree)
+    // always sits in shared memory.
+    const int path_bound = maxm * (maxm + 1) / 2 + 2 * capacity_of(f->bits);
+    const int cls_bytes = kernel_class_bytes(f->bits);
+    const int min_smem = f->bits <= 64 ? 64 : std::max(64, maxm + 1);
     int smem_classes = o.smem_classes;
-    int blocks = kernel_occupancy(f->wide, f->directed, 64);
+    int blocks = kernel_occupancy(f->bits, f->directed, min_smem);
     if (blocks <= 0) throw Error("search kernel cannot be resident on this device");
     if (smem_classes <= 0) {
         const int per_cta = ctx.smem_per_sm / blocks - 1024;
         const int per_warp = per_cta / kWarpsPerCta;
-        const int fixed = kernel_smem_per_warp(f->wide, f->directed, 0);
-        smem_classes = std::clamp((per_warp - fixed) / (f->wide ? 16 : 8), 64, 2048);
-        smem_classes = std::min(smem_classes, path_bound);
-        while (smem_classes > 64 && kernel_occupancy(f->wide, f->directed, smem_classes) < blocks)
+        const int fixed = kernel_smem_fixed(f->bits, f->directed);
+        smem_classes = std::clamp((per_warp - fixed) / cls_bytes, min_smem, 2048);
+        smem_classes = std::max(std::min(smem_classes, path_bound), min_smem);
+        while (smem_classes > min_smem && kernel_occupancy(f->bits, f->directed, smem_classes) < blocks)
             smem_classes -= 16;
     }
-    smem_classes = std::max(smem_classes, 64);
-    if (!f->wide) smem_classes = std::max(smem_classes, path_bound);  // 32-bit kernel: no spill path
-    blocks = kernel_occupancy(f->wide, f->directed, smem_classes);
+    smem_classes = std::max(smem_classes, min_smem);
+    if (f->bits == 32) smem_classes = std::max(smem_classes, path_bound);  // 32-bit kernel: no spill path
+    blocks = kernel_occupancy(f->bits, f->directed, smem_classes);
     if (blocks <= 0) throw Error("requested shared-memory class stack does not fit");
     int ctas = blocks * ctx.sms;
     if (o.max_warps > 0) ctas = std::min(ctas, (o.max_warps + kWarpsPerCta - 1) / kWarpsPerCta);
@@ -304,6 +339,8 @@ void plan(Context& ctx, const std::vector<Job>& jobs, const mcsg_options& o, InF
     f->ctas = std::max(ctas, 1);
     f->warps = f->ctas * kWarpsPerCta;
     f->smem_classes = smem_classes;
+    f->spill_classes = f->bits == 32 ? 0 : f->bits == 64 ? kSpillClasses : path_bound;
+    f->spill_bytes = size_t(f->spill_classes) * size_t(cls_bytes) * size_t(f->warps);
 }
 
 // Packs, stages and launches; returns without waiting.
@@ -321,13 +358,21 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
         for (Job& j : jobs) relabel_for_throughput(j, j.seed ? j.seed : o.seed);
     plan(ctx, jobs, o, &f);
     const int n = f.n;
-    ctx.reserve(size_t(n), size_t(n_groups), size_t(f.warps));
-    if (ex.seeded.size() + size_t(f.warps) > kRingCap) throw Error("too many seeded subtrees for the ring");
+    const bool wide = f.bits > 64;
+    ctx.reserve(size_t(n), size_t(n_groups), f.spill_bytes);
+    if (wide) ctx.reserve_wide(size_t(n));
+    const uint32_t ring_cap = wide ? kWideRingCap : kRingCap;
+    if (ex.seeded.size() + size_t(f.warps) > ring_cap) throw Error("too many seeded subtrees for the ring");
+    if (wide && !ex.seeded.empty()) throw Error("pre-seeded subtrees need n <= 64");
 
     f.t_stage = std::chrono::steady_clock::now();
     for (int i = 0; i < n; ++i) {
-        pack_instance(jobs[i].g, jobs[i].h, jobs[i].goal, o.disable_pruning == 0, jobs[i].floor_size,
-                      jobs[i].group, &ctx.h_inst[i]);
+        if (wide)
+            pack_wide(jobs[i].g, jobs[i].h, jobs[i].goal, o.disable_pruning == 0, jobs[i].floor_size,
+                      jobs[i].group, &ctx.h_winst[i]);
+        else
+            pack_instance(jobs[i].g, jobs[i].h, jobs[i].goal, o.disable_pruning == 0, jobs[i].floor_size,
+                          jobs[i].group, &ctx.h_inst[i]);
         std::memset(&ctx.h_ist[i], 0, sizeof(InstanceState));
         ctx.h_ist[i].open_tasks = ex.roots ? 1 : 0;
     }
@@ -342,7 +387,10 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
         ctx.h_grp[0].best = unsigned(ex.seed_best);
     }
     for (const TaskSlot& t : ex.seeded) ctx.h_ist[t.hdr.inst].open_tasks += 1;
-    ck(cudaMemcpyAsync(ctx.d_inst, ctx.h_inst, sizeof(InstanceDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    if (wide)
+        ck(cudaMemcpyAsync(ctx.d_winst, ctx.h_winst, sizeof(WideDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
+    else
+        ck(cudaMemcpyAsync(ctx.d_inst, ctx.h_inst, sizeof(InstanceDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_ist, ctx.h_ist, sizeof(InstanceState) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_grp, ctx.h_grp, sizeof(GroupState) * n_groups, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     *ctx.h_ctl = Ctl{};
@@ -350,7 +398,10 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     ctx.h_ctl->tail.v = ex.seeded.size();
     ctx.h_ctl->live.v = n;
     ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
-    ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
+    if (wide)
+        ck(ring_reset_wide(ctx.d_wslots, kWideRingCap, ctx.d_cnt, ctx.stream), "ring reset");
+    else
+        ck(ring_reset(ctx.d_slots, kRingCap, ctx.d_cnt, ctx.stream), "ring reset");
     if (!ex.seeded.empty()) {
         // published slots: sequence word = ticket + 1 (the consumer of ticket i reads it)
         std::vector<TaskSlot> staged(ex.seeded);
@@ -365,11 +416,13 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
 
     KernelParams p{};
     p.inst = ctx.d_inst;
+    p.winst = ctx.d_winst;
     p.ist = ctx.d_ist;
     p.grp = ctx.d_grp;
     p.slots = ctx.d_slots;
+    p.wslots = ctx.d_wslots;
     p.ctl = ctx.d_ctl;
-    p.cap_mask = kRingCap - 1;
+    p.cap_mask = ring_cap - 1;
     p.n_inst = n;
     p.n_roots = ex.roots ? n : 0;
     p.n_peers = int(ex.peers.size());
@@ -379,7 +432,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
     p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
     p.spill = ctx.d_spill;
-    p.spill_classes = f.wide ? kSpillClasses : 0;
+    p.spill_classes = f.spill_classes;
     p.smem_classes = f.smem_classes;
     p.donate = parity ? 0 : 1;
     p.poll_interval = parity ? 4096 : 256;
@@ -390,7 +443,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     }
 
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
-    ck(kernel_launch(f.wide, f.directed, parity, p, f.ctas, ctx.stream), "search kernel launch");
+    ck(kernel_launch(f.bits, f.directed, parity, p, f.ctas, ctx.stream), "search kernel launch");
     ck(cudaEventRecord(ctx.ev1, ctx.stream), "event");
     ck(cudaMemcpyAsync(ctx.h_ist, ctx.d_ist, sizeof(InstanceState) * n, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_grp, ctx.d_grp, sizeof(GroupState) * n_groups, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
@@ -423,9 +476,9 @@ LaunchOut finish(InFlight& f) {
     out.counters = *ctx.h_cnt;
     out.warps = f.warps;
     out.ctas = f.ctas;
-    out.smem_per_cta = kernel_smem_per_warp(f.wide, f.directed, f.smem_classes) * kWarpsPerCta;
+    out.smem_per_cta = kernel_smem_per_warp(f.bits, f.directed, f.smem_classes) * kWarpsPerCta;
     out.smem_classes = f.smem_classes;
-    out.h2d_bytes = (sizeof(InstanceDesc) + sizeof(InstanceState)) * uint64_t(n) +
+    out.h2d_bytes = ((f.bits > 64 ? sizeof(WideDesc) : sizeof(InstanceDesc)) + sizeof(InstanceState)) * uint64_t(n) +
                     sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl) + sizeof(TaskSlot) * f.seeded;
     out.d2h_bytes = sizeof(InstanceState) * uint64_t(n) + sizeof(GroupState) * uint64_t(n_groups) +
                     sizeof(Counters) + sizeof(Ctl);
@@ -526,7 +579,7 @@ std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_o
         oo.mode = MCSG_MODE_THROUGHPUT;
         plan(*ctxs[i], plans[i].jobs, oo, &shape);
         ck(cudaSetDevice(ctxs[i]->device), "cudaSetDevice");
-        ctxs[i]->reserve(plans[i].jobs.size(), 1, size_t(shape.warps));
+        ctxs[i]->reserve(plans[i].jobs.size(), 1, shape.spill_bytes);
     }
     std::vector<InFlight> fl(D);
     for (int i = 0; i < D; ++i) {
@@ -559,6 +612,8 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
     job.floor_size = o.floor_size;
     job.group = 0;
     relabel_for_throughput(job, o.seed);
+    if (std::max(job.g.n, job.h.n) > kMaxN)
+        throw Error("sharding one instance over devices needs n <= 64 (wide graphs run on one device)");
     InstanceDesc desc;
     pack_instance(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, &desc);
     const int per_dev = o.frontier > 0 ? o.frontier : 256;
@@ -678,8 +733,8 @@ mcsg_options defaults(const mcsg_options* o) {
 void check_pair(const HostGraph& g, const HostGraph& h) {
     if (g.directed != h.directed) throw Error("solve: graphs must share a kind");
     if (g.labeled != h.labeled) throw Error("cannot mix a labeled graph with an unlabeled one");
-    if (g.n > kMaxN || h.n > kMaxN)
-        throw Error("graphs above " + std::to_string(kMaxN) + " vertices are not supported");
+    if (g.n > kMaxWideN || h.n > kMaxWideN)
+        throw Error("graphs above " + std::to_string(kMaxWideN) + " vertices are not supported");
 }
 
 void write_result(const HostGraph& g, const HostGraph& h, const JobResult& r, mcsg_result* out) {
@@ -1153,6 +1208,24 @@ int32_t mcsg_pack_graph(const mcsg_graph* g, uint64_t* out_rows, uint64_t* in_ro
             out_rows[v] = d.out_g[v];
             if (in_rows) in_rows[v] = d.in_g[v];
         }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int32_t mcsg_pack_graph_words(const mcsg_graph* g, int32_t words, uint64_t* out_rows, uint64_t* in_rows) {
+    try {
+        const HostGraph x = HostGraph::from_abi(g);
+        if (x.n > kMaxWideN) throw Error("graph above " + std::to_string(kMaxWideN) + " vertices");
+        if (words < (x.n + 63) / 64 || words > kWideWords) throw Error("row width does not fit the graph");
+        auto d = std::make_unique<WideDesc>();
+        pack_wide(x, x, 0, true, 0, 0, d.get());
+        for (int v = 0; v < x.n; ++v)
+            for (int w = 0; w < words; ++w) {
+                out_rows[size_t(v) * words + w] = d->out_g[v][w];
+                if (in_rows) in_rows[size_t(v) * words + w] = d->in_g[v][w];
+            }
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

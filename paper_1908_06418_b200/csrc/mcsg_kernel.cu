@@ -35,13 +35,15 @@ namespace mcsg {
 // waiting; warps that finish a task take queued subtrees in ticket order.
 constexpr int kStarvedQueue = 256;
 
-template <typename W, bool DIR, bool PAR>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
+template <class X, bool PAR>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
     mcs_search_kernel(KernelParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    using Sm = WarpSmem<W, DIR>;
-    using X = Search<W, DIR>;
-    constexpr int NB = Bits<W>::n;
+    using Sm = typename X::Sm;
+    using W = typename X::Set;  // vertex bitset (one word, or WSet for wide graphs)
+    using Cl = Cls<W>;
+    using Slot = typename X::Slot;
+    constexpr int NB = X::NB;
     constexpr int P = X::P;
     const int lane = threadIdx.x & 31;
     // warp index via a warp reduction: the result lives in a uniform register,
@@ -49,18 +51,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
     // datapath instead of being rematerialised from SR_TID in the hot loop
     const int wib = int(__reduce_min_sync(kFull, threadIdx.x >> 5));
     const int gw = blockIdx.x * kWarpsPerCta + wib;
-    const int per_warp = warp_smem_bytes<W, DIR>(p.smem_classes);
+    const int per_warp = warp_smem_bytes<X>(p.smem_classes);
     Sm& s = *reinterpret_cast<Sm*>(smem_raw + size_t(wib) * per_warp);
-    X x{s,
-        reinterpret_cast<Cls<W>*>(smem_raw + size_t(wib) * per_warp + warp_smem_fixed<W, DIR>()),
-        reinterpret_cast<Cls<W>*>(p.spill) + size_t(gw) * p.spill_classes,
-        p.smem_classes,
-        lane,
-        lanemask_lt(),
-        {},
-        {},
-        {},
-        {}};
+    X x(s, reinterpret_cast<Cl*>(smem_raw + size_t(wib) * per_warp + warp_smem_fixed<X>()),
+        reinterpret_cast<Cl*>(p.spill) + size_t(gw) * p.spill_classes, p.smem_classes, lane, lanemask_lt());
+    Slot* const ring = X::slots(p);
     const int stack_limit = p.smem_classes + p.spill_classes;
     Ctl* const ctl = p.ctl;
     const int interval = p.poll_interval;
@@ -112,7 +107,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 }
                 int ok = 0;
                 if (lane == 0) {
-                    const TaskSlot* sl = p.slots + (ticket & p.cap_mask);
+                    const Slot* sl = ring + (ticket & p.cap_mask);
                     ok = ld_acquire(&sl->seq) == ticket + 1;
                 }
                 ok = __shfl_sync(kFull, ok, 0);
@@ -145,25 +140,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
         }
 
         // ---------------------------------------------------- load the task
-        TaskSlot* slot = nullptr;
+        Slot* slot = nullptr;
         TaskHeader hdr{};
         if (branch) {
-            slot = p.slots + (slot_pos & p.cap_mask);
+            slot = ring + (slot_pos & p.cap_mask);
             __syncwarp();
             hdr = slot->hdr;
             inst = hdr.inst;
         }
         if (inst != cur_inst) {
-            const InstanceDesc& dsc = p.inst[inst];
-            for (int i = lane; i < NB; i += 32) {
-                s.out_g[i] = W(dsc.out_g[i]);
-                s.out_h[i] = W(dsc.out_h[i]);
-                if constexpr (DIR) {
-                    s.in_g[i] = W(dsc.in_g[i]);
-                    s.in_h[i] = W(dsc.in_h[i]);
-                }
-                if constexpr (PAR) s.vkey[i] = dsc.vkey[i];
-            }
+            const auto& dsc = X::descs(p)[inst];
+            x.template load_instance<PAR>(dsc);
             maxp = dsc.maxp;
             goal = dsc.goal;
             prune = dsc.prune;
@@ -218,15 +205,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
         };
 
         int d, root, base = 0, nc, bound, sel = 0, v = 0;
-        W cand = 0;
+        W cand{};
         int cont = 0;
         unsigned key = kNoKey;
         bool have_key = false;
         bool at_next = false;  // true: resume the u loop of the task's level
         if (!branch) {
-            const InstanceDesc& dsc = p.inst[inst];
+            const auto& dsc = X::descs(p)[inst];
             nc = dsc.n_init;
-            for (int i = lane; i < nc; i += 32) x.scls[i] = Cls<W>{W(dsc.init_l[i]), W(dsc.init_r[i])};
+            x.load_root(dsc, nc);
             __syncwarp();
             d = root = 0;
             x.load_level(0, nc);
@@ -237,15 +224,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
         } else {
             d = root = hdr.depth;
             nc = hdr.nc;
-            for (int i = lane; i < nc; i += 32) x.scls[i] = Cls<W>{W(slot->cls_l[i]), W(slot->cls_r[i])};
-            for (int i = lane; i < d; i += 32) {
-                s.map_v[i] = slot->map_v[i];
-                s.map_u[i] = slot->map_u[i];
-            }
+            x.load_task(*slot, nc, d);
             sel = hdr.sel;
             v = hdr.v;
             bound = hdr.bound;
-            cand = W(hdr.cand);
+            cand = X::slot_cand(*slot);
             cont = hdr.cont;
             __syncwarp();
             if (lane == 0) st_release(&slot->seq, slot_pos + p.cap_mask + 1);  // free the slot
@@ -377,18 +360,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             for (int b0 = root; b0 < d && f < 0; b0 += 32) {
                 const int lv = b0 + lane;
                 bool has = false;
-                if (lv < d) has = s.f_cand[lv] != 0 || fr_cont(s.f_word[lv]);
+                if (lv < d) has = set_any(s.f_cand[lv]) || fr_cont(s.f_word[lv]);
                 const unsigned m = __ballot_sync(kFull, has);
                 if (m) f = b0 + __ffs(m) - 1;
             }
             if (f < 0) return true;
             const W fc = s.f_cand[f];
             const unsigned long long fw = s.f_word[f];
-            const int cnt = Bits<W>::popc(fc);
+            const int cnt = set_popc(fc);
             W give = fc;
             if (cnt >= 2)
-                for (int i = 0; i < (cnt + 1) / 2; ++i) give &= give - 1;  // upper half
-            const W keep = fc & ~give;
+                for (int i = 0; i < (cnt + 1) / 2; ++i) give = set_drop_lowest(give);  // upper half
+            const W keep = set_andnot(fc, give);
             // producer ticket; a warp is (probably) already waiting on it.
             // The slot is free once the consumer of ticket pos - cap released
             // it; the ring is far larger than the warp count, so this wait is
@@ -398,18 +381,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 atomicAdd(&ctl->pending.v, 1);
                 atomicAdd(&is->open_tasks, 1);
                 pos = atomicAdd(&ctl->tail.v, 1ull);
-                const TaskSlot* sl = p.slots + (pos & p.cap_mask);
+                const Slot* sl = ring + (pos & p.cap_mask);
                 while (ld_acquire(&sl->seq) != pos) __nanosleep(32);
             }
             pos = __shfl_sync(kFull, pos, 0);
-            TaskSlot* sl = p.slots + (pos & p.cap_mask);
+            Slot* sl = ring + (pos & p.cap_mask);
             const int fnc = fr_nc(fw);
-            const Cls<W>* fp = x.at(fr_base(fw));
-            for (int i = lane; i < fnc; i += 32) {
-                const Cls<W> c = fp[i];
-                sl->cls_l[i] = uint64_t(c.l);
-                sl->cls_r[i] = uint64_t(c.r);
-            }
+            x.store_task(*sl, fr_base(fw), fnc);
             for (int k = lane; k < f; k += 32) {
                 int mv, mu;
                 if (k < root) {
@@ -434,8 +412,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                 h.bound = uint8_t(fr_bound(fw));
                 h.cont = uint8_t(fr_cont(fw));
                 h.pad0 = 0;
-                h.cand = uint64_t(give);
                 h.pad1 = 0;
+                X::put_cand(*sl, h, give);
                 sl->hdr = h;
                 s.f_cand[f] = keep;
                 s.f_word[f] = fw & ~kFrameCont;  // the continuation left with the task
@@ -474,11 +452,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             // ---- the node survived its prune test: choose class and vertex
             if (!have_key) key = x.scan_key(nc, nullptr);
             if (key == kNoKey) goto pop;
-            sel = int(key & 127u);
+            sel = X::key_slot(key);
             {
                 const W lsel = x.class_l(sel);
                 if constexpr (PAR) v = x.select_vertex(lsel);
-                else v = Bits<W>::ctz(lsel);  // G is relabelled in select_vertex order
+                else v = set_ctz(lsel);  // G is relabelled in select_vertex order
                 cand = x.class_r(sel);
             }
             x.prep_v(v, sel);
@@ -486,9 +464,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
 
         next:
             // ---- u loop (search_core.hpp:183-200): children in ascending u
-            while (cand != 0) {
-                const int u = Bits<W>::ctz(cand);
-                cand &= cand - 1;
+            while (set_any(cand)) {
+                const int u = set_ctz(cand);
+                cand = set_drop_lowest(cand);
                 MCSG_COUNT_NODE();  // the child's entry
                 if (d + 1 > off_thr) {
                     offer(d, u);
@@ -510,7 +488,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
                         goto finish;
                     }
                 }
-                W h[P];
+                typename X::HParts h;
                 x.h_parts(u, h);
                 const int cbound = d + 1 + int(x.child_sum(u, h));
                 if (cbound <= prn_thr) continue;  // pruned at entry
@@ -549,33 +527,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
             // ---- v left unmatched (search_core.hpp:201-212): a counted node
             if (cont) {
                 MCSG_COUNT_NODE();
-                const W lsel = x.class_l(sel), rsel = x.class_r(sel);
-                bound -= (Bits<W>::popc(lsel) <= Bits<W>::popc(rsel)) ? 1 : 0;
-                const W nl = lsel & ~(W(1) << v);
-                Cls<W>* lvl = x.at(base);
-                if (nl != 0) {
-#pragma unroll
-                    for (int k = 0; k < X::S; ++k)
-                        if (lane + 32 * k == sel) x.L[k] = nl;
-                    if (lane == 0) lvl[sel].l = nl;
-                } else {
-                    // drop the emptied class: the last class takes its slot
-                    const W ll = x.class_l(nc - 1), lr = x.class_r(nc - 1);
-#pragma unroll
-                    for (int k = 0; k < X::S; ++k) {
-                        const int c = lane + 32 * k;
-                        if (c == nc - 1) {  // lanes past the level must hold empty classes
-                            x.L[k] = 0;
-                            x.R[k] = 0;
-                        }
-                        if (c == sel && sel != nc - 1) {
-                            x.L[k] = ll;
-                            x.R[k] = lr;
-                        }
-                    }
-                    if (lane == 0 && sel != nc - 1) lvl[sel] = Cls<W>{ll, lr};
-                    --nc;
-                }
+                x.cont_step(sel, v, nc, base, bound);
                 __syncwarp();
                 cont = 0;
                 have_key = false;
@@ -646,64 +598,77 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, (sizeof(W) == 4 ? 8 : 6))
 }
 
 // ------------------------------------------------------------ host launch --
-template <typename W, bool DIR, bool PAR>
+// Kernel flavours by bitset width: 32 (n <= 32), 64 (n <= 64), and the wide
+// policies 128 (n <= 128) and 256 (n <= 255).
+template <class X, bool PAR>
 static cudaError_t launch_t(const KernelParams& p, int ctas, cudaStream_t st) {
-    const int smem = warp_smem_bytes<W, DIR>(p.smem_classes) * kWarpsPerCta;
-    cudaError_t e = cudaFuncSetAttribute(mcs_search_kernel<W, DIR, PAR>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = warp_smem_bytes<X>(p.smem_classes) * kWarpsPerCta;
+    cudaError_t e = cudaFuncSetAttribute(mcs_search_kernel<X, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    mcs_search_kernel<W, DIR, PAR><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
+    mcs_search_kernel<X, PAR><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <typename W, bool DIR>
+template <class X>
 static int occupancy_t(int smem_classes) {
-    const int smem = warp_smem_bytes<W, DIR>(smem_classes) * kWarpsPerCta;
+    const int smem = warp_smem_bytes<X>(smem_classes) * kWarpsPerCta;
     int worst = 1 << 30;
     for (int par = 0; par < 2; ++par) {
-        auto fn = par ? mcs_search_kernel<W, DIR, true> : mcs_search_kernel<W, DIR, false>;
-        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-            return 0;
+        auto fn = par ? mcs_search_kernel<X, true> : mcs_search_kernel<X, false>;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kWarpsPerCta * 32, smem) !=
-            cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kWarpsPerCta * 32, smem) != cudaSuccess)
             return 0;
         worst = blocks < worst ? blocks : worst;
     }
     return worst;
 }
 
-int kernel_smem_per_warp(bool wide, bool directed, int smem_classes) {
-    if (wide) return directed ? warp_smem_bytes<uint64_t, true>(smem_classes)
-                              : warp_smem_bytes<uint64_t, false>(smem_classes);
-    return directed ? warp_smem_bytes<uint32_t, true>(smem_classes)
-                    : warp_smem_bytes<uint32_t, false>(smem_classes);
-}
-
-int kernel_occupancy(bool wide, bool directed, int smem_classes) {
-    if (wide) return directed ? occupancy_t<uint64_t, true>(smem_classes)
-                              : occupancy_t<uint64_t, false>(smem_classes);
-    return directed ? occupancy_t<uint32_t, true>(smem_classes)
-                    : occupancy_t<uint32_t, false>(smem_classes);
-}
-
-cudaError_t kernel_launch(bool wide, bool directed, bool parity, const KernelParams& p, int ctas,
-                          cudaStream_t st) {
-    if (parity) {
-        if (wide) return directed ? launch_t<uint64_t, true, true>(p, ctas, st)
-                                  : launch_t<uint64_t, false, true>(p, ctas, st);
-        return directed ? launch_t<uint32_t, true, true>(p, ctas, st)
-                        : launch_t<uint32_t, false, true>(p, ctas, st);
+// Calls f.template operator()<X>() with the policy of (bits, directed).
+template <class F>
+static auto with_policy(int bits, bool directed, F&& f) {
+    switch (bits) {
+        case 32:
+            return directed ? f.template operator()<Search<uint32_t, true>>()
+                            : f.template operator()<Search<uint32_t, false>>();
+        case 64:
+            return directed ? f.template operator()<Search<uint64_t, true>>()
+                            : f.template operator()<Search<uint64_t, false>>();
+        case 128:
+            return directed ? f.template operator()<WideSearch<2, true>>()
+                            : f.template operator()<WideSearch<2, false>>();
+        default:
+            return directed ? f.template operator()<WideSearch<4, true>>()
+                            : f.template operator()<WideSearch<4, false>>();
     }
-    if (wide) return directed ? launch_t<uint64_t, true, false>(p, ctas, st)
-                              : launch_t<uint64_t, false, false>(p, ctas, st);
-    return directed ? launch_t<uint32_t, true, false>(p, ctas, st)
-                    : launch_t<uint32_t, false, false>(p, ctas, st);
+}
+
+int kernel_smem_per_warp(int bits, bool directed, int smem_classes) {
+    return with_policy(bits, directed, [&]<class X>() { return warp_smem_bytes<X>(smem_classes); });
+}
+
+int kernel_smem_fixed(int bits, bool directed) {
+    return with_policy(bits, directed, [&]<class X>() { return warp_smem_fixed<X>(); });
+}
+
+int kernel_class_bytes(int bits) {
+    return bits == 32 ? 8 : bits == 64 ? 16 : bits == 128 ? 32 : 64;
+}
+
+int kernel_occupancy(int bits, bool directed, int smem_classes) {
+    return with_policy(bits, directed, [&]<class X>() { return occupancy_t<X>(smem_classes); });
+}
+
+cudaError_t kernel_launch(int bits, bool directed, bool parity, const KernelParams& p, int ctas, cudaStream_t st) {
+    return with_policy(bits, directed, [&]<class X>() {
+        return parity ? launch_t<X, true>(p, ctas, st) : launch_t<X, false>(p, ctas, st);
+    });
 }
 
 // Resets the ring (slot i of lap 0 expects producer ticket i) and the
 // per-launch counters. One thread per slot.
-__global__ void ring_reset_kernel(TaskSlot* slots, uint32_t cap, Counters* c) {
+template <class Slot>
+__global__ void ring_reset_kernel(Slot* slots, uint32_t cap, Counters* c) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap) slots[i].seq = i;
     if (i == 0) {
@@ -713,6 +678,11 @@ __global__ void ring_reset_kernel(TaskSlot* slots, uint32_t cap, Counters* c) {
 }
 
 cudaError_t ring_reset(TaskSlot* slots, uint32_t cap, Counters* c, cudaStream_t st) {
+    ring_reset_kernel<<<(cap + 255) / 256, 256, 0, st>>>(slots, cap, c);
+    return cudaGetLastError();
+}
+
+cudaError_t ring_reset_wide(WideSlot* slots, uint32_t cap, Counters* c, cudaStream_t st) {
     ring_reset_kernel<<<(cap + 255) / 256, 256, 0, st>>>(slots, cap, c);
     return cudaGetLastError();
 }

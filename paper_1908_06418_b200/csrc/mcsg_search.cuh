@@ -58,6 +58,81 @@ struct Bits<uint64_t> {
     __device__ static __forceinline__ int ctz(uint64_t x) { return __ffsll(x) - 1; }
 };
 
+// Bitset operations shared by the 32/64-bit kernels (one machine word) and
+// the wide kernels (WSet: NW 64-bit words, vertex v = bit v%64 of word v/64).
+template <int NW>
+struct alignas(16) WSet {
+    uint64_t w[NW];
+};
+
+template <typename W>
+__device__ __forceinline__ bool set_any(W x) { return x != 0; }
+template <typename W>
+__device__ __forceinline__ int set_ctz(W x) { return Bits<W>::ctz(x); }
+template <typename W>
+__device__ __forceinline__ int set_popc(W x) { return Bits<W>::popc(x); }
+template <typename W>
+__device__ __forceinline__ W set_drop_lowest(W x) { return x & (x - 1); }
+template <typename W>
+__device__ __forceinline__ W set_andnot(W a, W b) { return a & ~b; }
+
+template <int NW>
+__device__ __forceinline__ bool set_any(const WSet<NW>& x) {
+    uint64_t o = x.w[0];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) o |= x.w[i];
+    return o != 0;
+}
+template <int NW>
+__device__ __forceinline__ int set_popc(const WSet<NW>& x) {
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) c += __popcll(x.w[i]);
+    return c;
+}
+// lowest set bit (-1 when empty)
+template <int NW>
+__device__ __forceinline__ int set_ctz(const WSet<NW>& x) {
+    int r = -1;
+#pragma unroll
+    for (int i = NW - 1; i >= 0; --i)
+        if (x.w[i]) r = 64 * i + __ffsll(x.w[i]) - 1;
+    return r;
+}
+template <int NW>
+__device__ __forceinline__ WSet<NW> set_drop_lowest(WSet<NW> x) {
+    bool done = false;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        if (!done && x.w[i]) {
+            x.w[i] &= x.w[i] - 1;
+            done = true;
+        }
+    }
+    return x;
+}
+template <int NW>
+__device__ __forceinline__ WSet<NW> set_andnot(const WSet<NW>& a, const WSet<NW>& b) {
+    WSet<NW> r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.w[i] = a.w[i] & ~b.w[i];
+    return r;
+}
+template <int NW>
+__device__ __forceinline__ WSet<NW> set_and(const WSet<NW>& a, const WSet<NW>& b) {
+    WSet<NW> r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.w[i] = a.w[i] & b.w[i];
+    return r;
+}
+template <int NW>
+__device__ __forceinline__ WSet<NW> set_bit(int v) {
+    WSet<NW> r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.w[i] = (v >> 6) == i ? (1ull << (v & 63)) : 0ull;
+    return r;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -156,24 +231,37 @@ struct WarpSmem {
     uint8_t map_u[kMaxDepth + 1];
 };
 
-template <typename W, bool DIR>
+// Per-warp shared memory of a search policy X: its fixed image, then the
+// class stack.
+template <class X>
 __host__ __device__ constexpr int warp_smem_fixed() {
-    return (int)((sizeof(WarpSmem<W, DIR>) + 15) & ~size_t(15));
+    return (int)((sizeof(typename X::Sm) + 15) & ~size_t(15));
 }
 
-template <typename W, bool DIR>
+template <class X>
 __host__ __device__ constexpr int warp_smem_bytes(int classes) {
-    return (warp_smem_fixed<W, DIR>() + classes * int(sizeof(Cls<W>)) + 15) & ~15;
+    return (warp_smem_fixed<X>() + classes * int(sizeof(Cls<typename X::Set>)) + 15) & ~15;
 }
 
 // The per-warp search state held in registers plus its views of memory.
+//
+// The kernel body (mcsg_kernel.cu) is written against this policy interface;
+// WideSearch below implements the same interface for 64 < n <= 255.
 template <typename W, bool DIR>
 struct Search {
     static constexpr int S = Bits<W>::slots;
     static constexpr int NB = Bits<W>::n;
     static constexpr int P = DIR ? 4 : 2;  // split parts (codes 0..3 / 0..1)
+    static constexpr int kMinBlocks = sizeof(W) == 4 ? 8 : 6;  // __launch_bounds__
+    using Set = W;
+    using Sm = WarpSmem<W, DIR>;
+    using Desc = InstanceDesc;
+    using Slot = TaskSlot;
+    struct HParts {
+        W h[P];
+    };
 
-    WarpSmem<W, DIR>& s;
+    Sm& s;
     Cls<W>* scls;   // shared-memory class stack
     Cls<W>* gcls;   // HBM spill area (64-bit kernel)
     int cap;
@@ -189,6 +277,49 @@ struct Search {
 
     // slot k holds live classes (slot 0 always; slot 1 only when nc > 32)
     __device__ __forceinline__ bool live(int k) const { return k == 0 || two; }
+
+    __device__ __forceinline__ Search(Sm& s_, Cls<W>* scls_, Cls<W>* gcls_, int cap_, int lane_, unsigned lt_)
+        : s(s_), scls(scls_), gcls(gcls_), cap(cap_), lane(lane_), lt(lt_) {}
+
+    __device__ static __forceinline__ const Desc* descs(const KernelParams& p) { return p.inst; }
+    __device__ static __forceinline__ Slot* slots(const KernelParams& p) { return p.slots; }
+    __device__ static __forceinline__ int key_slot(unsigned key) { return int(key & 127u); }
+
+    // adjacency rows (and the parity-mode vertex keys) of a new instance
+    template <bool PAR>
+    __device__ __forceinline__ void load_instance(const Desc& d) {
+        for (int i = lane; i < NB; i += 32) {
+            s.out_g[i] = W(d.out_g[i]);
+            s.out_h[i] = W(d.out_h[i]);
+            if constexpr (DIR) {
+                s.in_g[i] = W(d.in_g[i]);
+                s.in_h[i] = W(d.in_h[i]);
+            }
+            if constexpr (PAR) s.vkey[i] = d.vkey[i];
+        }
+    }
+    // initial classes (label_classes.cpp:8-39) at stack position 0
+    __device__ __forceinline__ void load_root(const Desc& d, int nc) {
+        for (int i = lane; i < nc; i += 32) scls[i] = Cls<W>{W(d.init_l[i]), W(d.init_r[i])};
+    }
+    // a donated subtree: its classes at stack position 0, its mapping prefix
+    __device__ __forceinline__ void load_task(const Slot& sl, int nc, int d) {
+        for (int i = lane; i < nc; i += 32) scls[i] = Cls<W>{W(sl.cls_l[i]), W(sl.cls_r[i])};
+        for (int i = lane; i < d; i += 32) {
+            s.map_v[i] = sl.map_v[i];
+            s.map_u[i] = sl.map_u[i];
+        }
+    }
+    __device__ static __forceinline__ W slot_cand(const Slot& sl) { return W(sl.hdr.cand); }
+    __device__ __forceinline__ void store_task(Slot& sl, int fbase, int fnc) const {
+        const Cls<W>* fp = at(fbase);
+        for (int i = lane; i < fnc; i += 32) {
+            const Cls<W> c = fp[i];
+            sl.cls_l[i] = uint64_t(c.l);
+            sl.cls_r[i] = uint64_t(c.r);
+        }
+    }
+    __device__ static __forceinline__ void put_cand(Slot&, TaskHeader& h, W give) { h.cand = uint64_t(give); }
 
     // The 32-bit kernel never spills: the host sizes its shared stack to the
     // path bound m(m+1)/2. The 64-bit kernel keeps levels past `cap` in HBM;
@@ -278,7 +409,8 @@ struct Search {
             g[3] = ao & ai;
         }
     }
-    __device__ __forceinline__ void h_parts(int u, W h[P]) const {
+    __device__ __forceinline__ void h_parts(int u, HParts& hp) const {
+        W* h = hp.h;
         const W bo = s.out_h[u];
         if constexpr (!DIR) {
             h[0] = ~bo;
@@ -322,8 +454,9 @@ struct Search {
     // u is in no adjacency row of its own, so it only ever sits in part 0 of
     // the selected class: |R\{u} ∩ part_q| = |R ∩ part_q| for q > 0, and part
     // 0 follows from rs = |R| - [selected] by subtraction (no per-u masking).
-    __device__ __forceinline__ unsigned child_sum(int u, const W h[P]) const {
+    __device__ __forceinline__ unsigned child_sum(int u, const HParts& hp) const {
         (void)u;
+        const W* h = hp.h;
         unsigned sm = 0;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -348,9 +481,9 @@ struct Search {
     // filter_classes (label_classes.cpp:80-108): split every class by the
     // codes toward (v,u), drop one-sided parts, compact into the next level
     // with ballots; returns the child's class count and its best class key.
-    __device__ __forceinline__ int split(int u, int v, const W h[P], int cbase, unsigned* key_out) {
-        if (in_smem(cbase)) return split_into(u, v, h, scls + cbase, key_out);
-        return split_into(u, v, h, gcls + (cbase - cap), key_out);
+    __device__ __forceinline__ int split(int u, int v, const HParts& hp, int cbase, unsigned* key_out) {
+        if (in_smem(cbase)) return split_into(u, v, hp.h, scls + cbase, key_out);
+        return split_into(u, v, hp.h, gcls + (cbase - cap), key_out);
     }
 
     __device__ __forceinline__ int split_into(int u, int v, const W h[P], Cls<W>* q, unsigned* key_out) {
@@ -378,6 +511,312 @@ struct Search {
         }
         *key_out = __reduce_min_sync(kFull, key);
         return total;
+    }
+
+    // "v unmatched" (search_core.hpp:201-212): the bound drops by
+    // [|L*| <= |R*|], v leaves L* and an emptied class is dropped (the last
+    // class takes its slot), in registers and in the level's stack copy.
+    __device__ __forceinline__ void cont_step(int sel, int v, int& nc, int base, int& bound) {
+        const W lsel = class_l(sel), rsel = class_r(sel);
+        bound -= (Bits<W>::popc(lsel) <= Bits<W>::popc(rsel)) ? 1 : 0;
+        const W nl = lsel & ~(W(1) << v);
+        Cls<W>* lvl = at(base);
+        if (nl != 0) {
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+                if (lane + 32 * k == sel) L[k] = nl;
+            if (lane == 0) lvl[sel].l = nl;
+        } else {
+            const W ll = class_l(nc - 1), lr = class_r(nc - 1);
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+                const int c = lane + 32 * k;
+                if (c == nc - 1) {  // lanes past the level must hold empty classes
+                    L[k] = 0;
+                    R[k] = 0;
+                }
+                if (c == sel && sel != nc - 1) {
+                    L[k] = ll;
+                    R[k] = lr;
+                }
+            }
+            if (lane == 0 && sel != nc - 1) lvl[sel] = Cls<W>{ll, lr};
+            --nc;
+        }
+    }
+};
+
+// ------------------------------------------------------------- wide graphs --
+// 64 < n <= 255: a bitset is NW 64-bit words (NW = 2: n <= 128, NW = 4:
+// n <= 255). A class no longer fits a lane's registers, and a level can hold
+// up to 255 classes, so the wide policy keeps every level in memory (the
+// per-warp shared-memory stack, spilling to HBM) and walks it 32 classes per
+// pass, lane = class. The per-class counts that every u candidate of a level
+// reuses (|LX ∩ part|, |R| - [selected]) are computed once per level into a
+// shared-memory scratch. Adjacency rows are read through the read-only data
+// path (L1), not staged: 255 rows × 32 B × 4 row sets would leave no room
+// for resident warps.
+template <int NW, bool DIR>
+struct WideSmem {
+    static constexpr int NB = NW >= 4 ? kMaxWideN : NW * 64;  // vertex capacity
+    static constexpr int P = DIR ? 4 : 2;
+    unsigned long long f_word[NB + 1];
+    alignas(16) uint32_t pf[24];
+    unsigned long long polled;
+    unsigned long long st_nodes, st_splits, st_donations, st_tasks, st_spills;
+    unsigned long long st_idle, st_busy;
+    WSet<NW> f_cand[NB + 1];
+    uint32_t vkey[NB];
+    uint8_t map_v[NB + 1];
+    uint8_t map_u[NB + 1];
+    uint8_t lcs[NB][P];  // |LX ∩ part_q(v)| of each class of the current level
+    uint8_t rss[NB];     // |R| - [class == selected]
+};
+
+template <int NW, bool DIR>
+struct WideSearch {
+    using Set = WSet<NW>;
+    using C = Cls<Set>;
+    using Sm = WideSmem<NW, DIR>;
+    using Desc = WideDesc;
+    using Slot = WideSlot;
+    static constexpr int NB = Sm::NB;
+    static constexpr int P = DIR ? 4 : 2;
+    static constexpr int kMinBlocks = 2;
+    struct HParts {
+        Set o, i;  // H rows of u (out; in when directed)
+    };
+
+    Sm& s;
+    C* scls;
+    C* gcls;
+    int cap;
+    int lane;
+    unsigned lt;
+    const Desc* dsc = nullptr;
+    C* lvl = nullptr;  // current level
+    int lnc = 0;
+    Set vb, go, gi;    // bit of v, G rows of v
+
+    __device__ __forceinline__ WideSearch(Sm& s_, C* scls_, C* gcls_, int cap_, int lane_, unsigned lt_)
+        : s(s_), scls(scls_), gcls(gcls_), cap(cap_), lane(lane_), lt(lt_) {}
+
+    __device__ static __forceinline__ const Desc* descs(const KernelParams& p) { return p.winst; }
+    __device__ static __forceinline__ Slot* slots(const KernelParams& p) { return p.wslots; }
+    __device__ static __forceinline__ int key_slot(unsigned key) { return int(key & 255u); }
+
+    // select_label_class key: (max, min, lowest left id, slot), 8 bits each
+    __device__ static __forceinline__ unsigned class_key(int pl, int pr, const Set& l, int slot) {
+        const unsigned mx = max(pl, pr), mn = min(pl, pr);
+        return (mx << 24) | (mn << 16) | (unsigned(set_ctz(l)) << 8) | unsigned(slot);
+    }
+
+    __device__ static __forceinline__ Set row(const uint64_t (*rows)[kWideWords], int v) {
+        Set x;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) x.w[i] = __ldg(&rows[v][i]);
+        return x;
+    }
+    // part q of a vertex's code row: undirected {¬adj, adj}; directed by
+    // (out bit, in bit): {neither, out only, in only, both}
+    __device__ static __forceinline__ Set part(int q, const Set& o, const Set& in) {
+        Set r;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const uint64_t a = o.w[i], b = DIR ? in.w[i] : 0ull;
+            r.w[i] = q == 0 ? ~(a | b) : q == 1 ? (a & ~b) : q == 2 ? (b & ~a) : (a & b);
+        }
+        return r;
+    }
+
+    __device__ __forceinline__ bool in_smem(int base) const { return base < cap; }
+    __device__ __forceinline__ C* at(int base) const { return in_smem(base) ? scls + base : gcls + (base - cap); }
+
+    template <bool PAR>
+    __device__ __forceinline__ void load_instance(const Desc& d) {
+        dsc = &d;
+        if constexpr (PAR)
+            for (int i = lane; i < NB; i += 32) s.vkey[i] = d.vkey[i];
+    }
+    __device__ static __forceinline__ C from_words(const uint64_t* l, const uint64_t* r) {
+        C c;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            c.l.w[i] = l[i];
+            c.r.w[i] = r[i];
+        }
+        return c;
+    }
+    // the host keeps every level-0 level in shared memory (cap > NB)
+    __device__ __forceinline__ void load_root(const Desc& d, int nc) {
+        for (int i = lane; i < nc; i += 32) scls[i] = from_words(d.init_l[i], d.init_r[i]);
+    }
+    __device__ __forceinline__ void load_task(const Slot& sl, int nc, int d) {
+        for (int i = lane; i < nc; i += 32) scls[i] = from_words(sl.cls[i][0], sl.cls[i][1]);
+        for (int i = lane; i < d; i += 32) {
+            s.map_v[i] = sl.map_v[i];
+            s.map_u[i] = sl.map_u[i];
+        }
+    }
+    __device__ static __forceinline__ Set slot_cand(const Slot& sl) {
+        Set x;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) x.w[i] = sl.cand[i];
+        return x;
+    }
+    __device__ __forceinline__ void store_task(Slot& sl, int fbase, int fnc) const {
+        const C* fp = at(fbase);
+        for (int i = lane; i < fnc; i += 32) {
+            const C c = fp[i];
+#pragma unroll
+            for (int k = 0; k < kWideWords; ++k) {
+                sl.cls[i][0][k] = k < NW ? c.l.w[k < NW ? k : 0] : 0ull;
+                sl.cls[i][1][k] = k < NW ? c.r.w[k < NW ? k : 0] : 0ull;
+            }
+        }
+    }
+    __device__ static __forceinline__ void put_cand(Slot& sl, TaskHeader& h, const Set& give) {
+        h.cand = 0;
+#pragma unroll
+        for (int k = 0; k < kWideWords; ++k) sl.cand[k] = k < NW ? give.w[k < NW ? k : 0] : 0ull;
+    }
+
+    __device__ __forceinline__ void load_level(int base, int nc) {
+        lvl = at(base);
+        lnc = nc;
+    }
+
+    // compute_bound + select_label_class over the level
+    __device__ __forceinline__ unsigned scan_key(int nc, unsigned* sum) const {
+        unsigned key = kNoKey, sm = 0;
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int c = c0 + lane;
+            if (c < nc) {
+                const C x = lvl[c];
+                const int pl = set_popc(x.l), pr = set_popc(x.r);
+                sm += unsigned(min(pl, pr));
+                key = min(key, class_key(pl, pr, x.l, c));
+            }
+        }
+        if (sum) *sum = __reduce_add_sync(kFull, sm);
+        return __reduce_min_sync(kFull, key);
+    }
+
+    // select_vertex (label_classes.cpp:69-78) over the vertex keys of L*
+    __device__ __forceinline__ int select_vertex(const Set& lsel) const {
+        unsigned k = kNoKey;
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int xb = lane + 32 * h, id = 64 * i + xb;
+                if (id < NB && ((lsel.w[i] >> xb) & 1ull)) k = min(k, s.vkey[id]);
+            }
+        return int(__reduce_min_sync(kFull, k) & 255u);
+    }
+
+    __device__ __forceinline__ Set class_l(int c) const { return lvl[c].l; }
+    __device__ __forceinline__ Set class_r(int c) const { return lvl[c].r; }
+
+    __device__ __forceinline__ void prep_v(int v, int sel) {
+        go = row(dsc->out_g, v);
+        if constexpr (DIR) gi = row(dsc->in_g, v);
+        vb = set_bit<NW>(v);
+        for (int c0 = 0; c0 < lnc; c0 += 32) {
+            const int c = c0 + lane;
+            if (c < lnc) {
+                const C x = lvl[c];
+                const Set lx = set_andnot(x.l, vb);
+                if constexpr (!DIR) {
+                    const int a = set_popc(set_and(lx, go));
+                    s.lcs[c][1] = uint8_t(a);
+                    s.lcs[c][0] = uint8_t(set_popc(lx) - a);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < P; ++q) s.lcs[c][q] = uint8_t(set_popc(set_and(lx, part(q, go, gi))));
+                }
+                s.rss[c] = uint8_t(set_popc(x.r) - (c == sel ? 1 : 0));
+            }
+        }
+        __syncwarp();
+    }
+
+    __device__ __forceinline__ void h_parts(int u, HParts& h) const {
+        h.o = row(dsc->out_h, u);
+        if constexpr (DIR) h.i = row(dsc->in_h, u);
+    }
+
+    // bound of the child minus |M|+1 (see Search::child_sum)
+    __device__ __forceinline__ unsigned child_sum(int u, const HParts& h) const {
+        (void)u;
+        unsigned sm = 0;
+        for (int c0 = 0; c0 < lnc; c0 += 32) {
+            const int c = c0 + lane;
+            if (c < lnc) {
+                const Set r = lvl[c].r;
+                const int rs = s.rss[c];
+                if constexpr (!DIR) {
+                    const int b = set_popc(set_and(r, h.o));
+                    sm += unsigned(min(int(s.lcs[c][0]), rs - b) + min(int(s.lcs[c][1]), b));
+                } else {
+                    int rest = rs;
+#pragma unroll
+                    for (int q = 1; q < P; ++q) {
+                        const int b = set_popc(set_and(r, part(q, h.o, h.i)));
+                        rest -= b;
+                        sm += unsigned(min(int(s.lcs[c][q]), b));
+                    }
+                    sm += unsigned(min(int(s.lcs[c][0]), rest));
+                }
+            }
+        }
+        return __reduce_add_sync(kFull, sm);
+    }
+
+    // filter_classes (label_classes.cpp:80-108) into the next level at cbase
+    __device__ __forceinline__ int split(int u, int v, const HParts& h, int cbase, unsigned* key_out) {
+        (void)v;
+        C* q = at(cbase);
+        const Set ub = set_bit<NW>(u);
+        int total = 0;
+        unsigned key = kNoKey;
+        for (int c0 = 0; c0 < lnc; c0 += 32) {
+            const int c = c0 + lane;
+            C x{};
+            if (c < lnc) x = lvl[c];
+            const Set lx = set_andnot(x.l, vb), rx = set_andnot(x.r, ub);
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) {
+                const Set lp = set_and(lx, part(pp, go, gi)), rp = set_and(rx, part(pp, h.o, h.i));
+                const bool keep = set_any(lp) & set_any(rp);
+                const unsigned m = __ballot_sync(kFull, keep);
+                if (keep) {
+                    const int pos = total + __popc(m & lt);
+                    q[pos] = C{lp, rp};
+                    key = min(key, class_key(set_popc(lp), set_popc(rp), lp, pos));
+                }
+                total += __popc(m);
+            }
+        }
+        *key_out = __reduce_min_sync(kFull, key);
+        return total;
+    }
+
+    // "v unmatched" (search_core.hpp:201-212), in the level's memory
+    __device__ __forceinline__ void cont_step(int sel, int v, int& nc, int base, int& bound) {
+        (void)base;
+        const C cs = lvl[sel], last = lvl[nc - 1];
+        __syncwarp();  // every lane has read the level before lane 0 rewrites it
+        bound -= (set_popc(cs.l) <= set_popc(cs.r)) ? 1 : 0;
+        const Set nl = set_andnot(cs.l, set_bit<NW>(v));
+        if (set_any(nl)) {
+            if (lane == 0) lvl[sel].l = nl;
+        } else {
+            if (lane == 0 && sel != nc - 1) lvl[sel] = last;
+            --nc;
+        }
+        __syncwarp();
+        lnc = nc;
     }
 };
 

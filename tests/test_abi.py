@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
             "mcsg_bound_jump", "mcsg_portfolio", "mcsg_verify", "mcsg_load_graph_file"} <= set(syms)
     for name in syms:
         assert hasattr(lib, name), f"{name} declared in include/mcsg.h but not exported"
-    assert M.lib().mcsg_abi_version() == 1
+    assert M.lib().mcsg_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
@@ -152,6 +152,33 @@ def test_pack_graph_rows():
             c = g.code(v, x)
             assert ((int(out[v]) >> x) & 1) == (c & 1)
             assert ((int(inn[v]) >> x) & 1) == ((c >> 1) & 1)
+
+
+@pytest.mark.parametrize("n,words", [(65, 2), (128, 2), (129, 3), (200, 4), (255, 4)])
+def test_pack_graph_words_rows(n, words):
+    # multi-word rows of the wide kernels: bit x%64 of word x//64
+    g = M.random_graph(n, 0.3, 50000 + n, directed=True, label_count=3)
+    out, inn = M.pack_graph_words(g, words)
+    assert out.shape == (n, words) and inn.shape == (n, words)
+    codes = g.codes
+    for v in range(0, n, 7):
+        for x in range(n):
+            c = int(codes[v, x])
+            assert ((int(out[v, x // 64]) >> (x % 64)) & 1) == (c & 1)
+            assert ((int(inn[v, x // 64]) >> (x % 64)) & 1) == ((c >> 1) & 1)
+    with pytest.raises(M.GraphError):
+        M.pack_graph_words(g, (n + 63) // 64 - 1)  # row too narrow
+
+
+def test_graph_size_limits():
+    # n <= 255 (vertex ids, class counts and bounds are bytes, like the
+    # reference's byte-frame engine: K254 accepted / K255 rejected there,
+    # test_engine_iterative.cpp:40-59); n = 256 is rejected before any launch
+    g = M.random_graph(256, 0.1, 3)
+    with pytest.raises(M.GraphError, match="255"):
+        M.solve(g, g)
+    with pytest.raises(M.GraphError, match="255"):
+        M.pack_graph_words(g, 4)
 
 
 def test_engine_spec_grammar():

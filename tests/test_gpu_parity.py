@@ -155,7 +155,7 @@ def test_errors_and_statuses():
     lab = M.random_graph(5, 0.5, 1, label_count=2)
     with pytest.raises(M.GraphError):
         M.solve(und, lab)
-    big = M.random_graph(65, 0.5, 1)
+    big = M.random_graph(256, 0.5, 1)  # n <= 255 (test_gpu_wide.py covers 65..255)
     with pytest.raises(M.GraphError):
         M.solve(big, big)
     g, h = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
