@@ -20,11 +20,10 @@ stalls = {k.replace('smsp__pcsamp_warps_issue_stalled_', ''): f(k) for k in hdr
           if k.startswith('smsp__pcsamp_warps_issue_stalled_') and not k.endswith('not_issued')}
 tot = sum(v for v in stalls.values() if v)
 out['warp_inst_per_node'] = out['smsp__inst_executed.sum'] / nodes
-dram = (out['dram__bytes_read.sum'] or 0) + (out['dram__bytes_write.sum'] or 0)
-if out['unit'].get('dram__bytes_read.sum') == 'Mbyte': dram *= 1e6
-elif out['unit'].get('dram__bytes_read.sum') == 'Gbyte': dram *= 1e9
-elif out['unit'].get('dram__bytes_read.sum') == 'Kbyte': dram *= 1e3
-out['dram_bytes_per_launch'] = dram
+SCALE = {'byte': 1.0, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}
+def nbytes(k):  # each metric carries its own unit
+    return (out[k] or 0.0) * SCALE.get(out['unit'].get(k), 1.0)
+out['dram_bytes_per_launch'] = nbytes('dram__bytes_read.sum') + nbytes('dram__bytes_write.sum')
 out['nodes_per_launch'] = nodes
 out['stall_pct'] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0)) if v}
 out['pipes_pct'] = {k.replace('sm__inst_executed_pipe_', '').replace('.avg.pct_of_peak_sustained_active', ''): v
