@@ -10,6 +10,8 @@
 // SearchTasks (engine_parallel.cpp:86-117, task_queue.hpp:27-48) and the
 // node rules of search_core.hpp:120-213 / label_classes.cpp:41-108.
 #include <algorithm>
+#include <array>
+#include <tuple>
 #include <cstring>
 #include <deque>
 
@@ -18,11 +20,33 @@
 namespace mcsg {
 namespace {
 
-inline int popc(uint64_t x) { return __builtin_popcountll(x); }
-inline int ctz(uint64_t x) { return __builtin_ctzll(x); }
+// Host bitset over up to 256 vertices (one word when n <= 64).
+using HSet = std::array<uint64_t, kWideWords>;
+
+inline int popc(const HSet& x) {
+    int c = 0;
+    for (uint64_t w : x) c += __builtin_popcountll(w);
+    return c;
+}
+inline int ctz(const HSet& x) {
+    for (int i = 0; i < kWideWords; ++i)
+        if (x[i]) return 64 * i + __builtin_ctzll(x[i]);
+    return -1;
+}
+inline bool any(const HSet& x) { return (x[0] | x[1] | x[2] | x[3]) != 0; }
+inline HSet band(const HSet& a, const HSet& b) { return {a[0] & b[0], a[1] & b[1], a[2] & b[2], a[3] & b[3]}; }
+inline HSet bnot(const HSet& a) { return {~a[0], ~a[1], ~a[2], ~a[3]}; }
+inline HSet without(HSet a, int v) {
+    a[v >> 6] &= ~(1ull << (v & 63));
+    return a;
+}
+
+// Rows and vertex keys of either description, as host sets.
+inline HSet set_of(uint64_t x) { return {x, 0, 0, 0}; }
+inline HSet set_of(const uint64_t (&x)[kWideWords]) { return {x[0], x[1], x[2], x[3]}; }
 
 struct Node {
-    std::vector<std::pair<uint64_t, uint64_t>> cls;
+    std::vector<std::pair<HSet, HSet>> cls;
     std::vector<uint8_t> mv, mu;
     int bound = 0;
 };
@@ -30,14 +54,9 @@ struct Node {
 struct Branch {
     Node node;
     int sel = 0, v = 0;
-    uint64_t cand = 0;
+    HSet cand{};
     int cont = 1;
 };
-
-unsigned class_key(int pl, int pr, uint64_t l, int slot) {
-    const unsigned mx = std::max(pl, pr), mn = std::min(pl, pr);
-    return (mx << 20) | (mn << 13) | (unsigned(ctz(l)) << 7) | unsigned(slot);
-}
 
 int bound_of(const Node& n) {
     int b = int(n.mv.size());
@@ -46,19 +65,24 @@ int bound_of(const Node& n) {
 }
 
 // select_label_class + select_vertex (label_classes.cpp:47-78) on a node that
-// survived its prune test; false when no class remains.
-bool enter(Node n, const InstanceDesc& d, Branch* out) {
-    unsigned best = ~0u;
+// survived its prune test; false when no class remains. The class order is
+// the kernel's key order: (max(|L|,|R|), min, lowest left id, slot).
+template <class D>
+bool enter(Node n, const D& d, Branch* out) {
+    std::tuple<int, int, int, int> best{1 << 30, 0, 0, 0};
     int sel = -1;
     for (int i = 0; i < int(n.cls.size()); ++i) {
-        const unsigned k = class_key(popc(n.cls[i].first), popc(n.cls[i].second), n.cls[i].first, i);
+        const int pl = popc(n.cls[i].first), pr = popc(n.cls[i].second);
+        const std::tuple<int, int, int, int> k{std::max(pl, pr), std::min(pl, pr), ctz(n.cls[i].first), i};
         if (k < best) best = k, sel = i;
     }
     if (sel < 0) return false;
-    const uint64_t l = n.cls[sel].first;
-    unsigned vk = ~0u;
-    for (uint64_t m = l; m; m &= m - 1) vk = std::min(vk, unsigned(d.vkey[ctz(m)]));
-    out->v = int(vk & 63u);
+    HSet l = n.cls[sel].first;
+    uint32_t vk = ~0u;
+    int v = -1;
+    for (int x = ctz(l); x >= 0; l = without(l, x), x = ctz(l))
+        if (uint32_t(d.vkey[x]) < vk) vk = uint32_t(d.vkey[x]), v = x;
+    out->v = v;
     out->sel = sel;
     out->cand = n.cls[sel].second;
     out->cont = 1;
@@ -67,28 +91,29 @@ bool enter(Node n, const InstanceDesc& d, Branch* out) {
 }
 
 // filter_classes (label_classes.cpp:80-108) for the child (v,u).
-Node child_of(const Branch& b, int u, const InstanceDesc& d, bool directed) {
+template <class D>
+Node child_of(const Branch& b, int u, const D& d, bool directed) {
     Node c;
     c.mv = b.node.mv;
     c.mu = b.node.mu;
     c.mv.push_back(uint8_t(b.v));
     c.mu.push_back(uint8_t(u));
-    const uint64_t ao = d.out_g[b.v], ai = d.in_g[b.v], bo = d.out_h[u], bi = d.in_h[u];
-    uint64_t gp[4], hp[4];
+    const HSet ao = set_of(d.out_g[b.v]), ai = set_of(d.in_g[b.v]);
+    const HSet bo = set_of(d.out_h[u]), bi = set_of(d.in_h[u]);
+    HSet gp[4], hp[4];
     int parts = 2;
     if (!directed) {
-        gp[0] = ~ao, gp[1] = ao, hp[0] = ~bo, hp[1] = bo;
+        gp[0] = bnot(ao), gp[1] = ao, hp[0] = bnot(bo), hp[1] = bo;
     } else {
         parts = 4;
-        gp[0] = ~(ao | ai), gp[1] = ao & ~ai, gp[2] = ai & ~ao, gp[3] = ao & ai;
-        hp[0] = ~(bo | bi), hp[1] = bo & ~bi, hp[2] = bi & ~bo, hp[3] = bo & bi;
+        gp[0] = band(bnot(ao), bnot(ai)), gp[1] = band(ao, bnot(ai)), gp[2] = band(ai, bnot(ao)), gp[3] = band(ao, ai);
+        hp[0] = band(bnot(bo), bnot(bi)), hp[1] = band(bo, bnot(bi)), hp[2] = band(bi, bnot(bo)), hp[3] = band(bo, bi);
     }
-    const uint64_t vb = 1ull << b.v, ub = 1ull << u;
     for (const auto& cl : b.node.cls) {
-        const uint64_t l = cl.first & ~vb, r = cl.second & ~ub;
+        const HSet l = without(cl.first, b.v), r = without(cl.second, u);
         for (int q = 0; q < parts; ++q) {
-            const uint64_t lp = l & gp[q], rp = r & hp[q];
-            if (lp && rp) c.cls.push_back({lp, rp});
+            const HSet lp = band(l, gp[q]), rp = band(r, hp[q]);
+            if (any(lp) && any(rp)) c.cls.push_back({lp, rp});
         }
     }
     c.bound = bound_of(c);
@@ -100,8 +125,8 @@ Node continuation_of(const Branch& b) {
     Node c = b.node;
     const auto cl = c.cls[b.sel];
     c.bound -= popc(cl.first) <= popc(cl.second) ? 1 : 0;
-    const uint64_t nl = cl.first & ~(1ull << b.v);
-    if (nl) {
+    const HSet nl = without(cl.first, b.v);
+    if (any(nl)) {
         c.cls[b.sel].first = nl;
     } else {
         c.cls[b.sel] = c.cls.back();
@@ -110,9 +135,8 @@ Node continuation_of(const Branch& b) {
     return c;
 }
 
-TaskSlot to_slot(const Branch& b, int inst) {
-    TaskSlot s;
-    std::memset(&s, 0, sizeof(s));
+template <class S>
+void fill_header(S& s, const Branch& b, int inst) {
     s.hdr.inst = inst;
     s.hdr.kind = kTaskBranch;
     s.hdr.depth = uint8_t(b.node.mv.size());
@@ -121,24 +145,42 @@ TaskSlot to_slot(const Branch& b, int inst) {
     s.hdr.v = uint8_t(b.v);
     s.hdr.bound = uint8_t(b.node.bound);
     s.hdr.cont = uint8_t(b.cont);
-    s.hdr.cand = b.cand;
     for (size_t k = 0; k < b.node.mv.size(); ++k) {
         s.map_v[k] = b.node.mv[k];
         s.map_u[k] = b.node.mu[k];
     }
-    for (size_t i = 0; i < b.node.cls.size(); ++i) {
-        s.cls_l[i] = b.node.cls[i].first;
-        s.cls_r[i] = b.node.cls[i].second;
-    }
-    return s;
 }
 
-}  // namespace
+void push_slot(const Branch& b, int inst, Frontier* f, const InstanceDesc&) {
+    TaskSlot s;
+    std::memset(&s, 0, sizeof(s));
+    fill_header(s, b, inst);
+    s.hdr.cand = b.cand[0];
+    for (size_t i = 0; i < b.node.cls.size(); ++i) {
+        s.cls_l[i] = b.node.cls[i].first[0];
+        s.cls_r[i] = b.node.cls[i].second[0];
+    }
+    f->tasks.push_back(s);
+}
 
-Frontier expand_frontier(const InstanceDesc& d, bool directed, int target, int inst) {
+void push_slot(const Branch& b, int inst, Frontier* f, const WideDesc&) {
+    f->wtasks.emplace_back();
+    WideSlot& s = f->wtasks.back();
+    std::memset(&s, 0, sizeof(s));
+    fill_header(s, b, inst);
+    for (int w = 0; w < kWideWords; ++w) s.cand[w] = b.cand[w];
+    for (size_t i = 0; i < b.node.cls.size(); ++i)
+        for (int w = 0; w < kWideWords; ++w) {
+            s.cls[i][0][w] = b.node.cls[i].first[w];
+            s.cls[i][1][w] = b.node.cls[i].second[w];
+        }
+}
+
+template <class D>
+Frontier expand(const D& d, bool directed, int target, int inst) {
     Frontier f;
     Node root;
-    for (int i = 0; i < d.n_init; ++i) root.cls.push_back({d.init_l[i], d.init_r[i]});
+    for (int i = 0; i < d.n_init; ++i) root.cls.push_back({set_of(d.init_l[i]), set_of(d.init_r[i])});
     root.bound = bound_of(root);
     f.nodes = 1;
     // The host keeps its own incumbent from the mappings it passes through:
@@ -155,7 +197,7 @@ Frontier expand_frontier(const InstanceDesc& d, bool directed, int target, int i
         Branch b = std::move(open.front());
         open.pop_front();
         const int depth = int(b.node.mv.size());
-        for (uint64_t m = b.cand; m; m &= m - 1) {
+        for (HSet m = b.cand; any(m); m = without(m, ctz(m))) {
             const int u = ctz(m);
             Node c = child_of(b, u, d, directed);
             ++f.nodes;
@@ -185,8 +227,18 @@ Frontier expand_frontier(const InstanceDesc& d, bool directed, int target, int i
         }
     }
     f.best_size = best;
-    for (const Branch& b : open) f.tasks.push_back(to_slot(b, inst));
+    for (const Branch& b : open) push_slot(b, inst, &f, d);
     return f;
+}
+
+}  // namespace
+
+Frontier expand_frontier(const InstanceDesc& d, bool directed, int target, int inst) {
+    return expand(d, directed, target, inst);
+}
+
+Frontier expand_frontier(const WideDesc& d, bool directed, int target, int inst) {
+    return expand(d, directed, target, inst);
 }
 
 }  // namespace mcsg

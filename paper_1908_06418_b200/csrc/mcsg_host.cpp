@@ -274,6 +274,7 @@ double secs_since(std::chrono::steady_clock::time_point t0) {
 // What a launch does beyond "every instance is a root task".
 struct LaunchExtras {
     std::vector<TaskSlot> seeded;    // subtrees published in the ring before the launch
+    std::vector<WideSlot> wseeded;   // the same for a wide (n > 64) launch
     bool roots = true;               // hand out every instance as a root task
     std::vector<GroupState*> peers;  // group 0's incumbent on the other devices (P2P)
     bool peer_done_on_complete = false;
@@ -362,8 +363,9 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     ctx.reserve(size_t(n), size_t(n_groups), f.spill_bytes);
     if (wide) ctx.reserve_wide(size_t(n));
     const uint32_t ring_cap = wide ? kWideRingCap : kRingCap;
-    if (ex.seeded.size() + size_t(f.warps) > ring_cap) throw Error("too many seeded subtrees for the ring");
-    if (wide && !ex.seeded.empty()) throw Error("pre-seeded subtrees need n <= 64");
+    const size_t n_seeded = wide ? ex.wseeded.size() : ex.seeded.size();
+    if (n_seeded + size_t(f.warps) > ring_cap) throw Error("too many seeded subtrees for the ring");
+    if (wide ? !ex.seeded.empty() : !ex.wseeded.empty()) throw Error("seeded subtrees of the wrong width");
 
     f.t_stage = std::chrono::steady_clock::now();
     for (int i = 0; i < n; ++i) {
@@ -387,6 +389,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
         ctx.h_grp[0].best = unsigned(ex.seed_best);
     }
     for (const TaskSlot& t : ex.seeded) ctx.h_ist[t.hdr.inst].open_tasks += 1;
+    for (const WideSlot& t : ex.wseeded) ctx.h_ist[t.hdr.inst].open_tasks += 1;
     if (wide)
         ck(cudaMemcpyAsync(ctx.d_winst, ctx.h_winst, sizeof(WideDesc) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     else
@@ -394,8 +397,8 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     ck(cudaMemcpyAsync(ctx.d_ist, ctx.h_ist, sizeof(InstanceState) * n, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     ck(cudaMemcpyAsync(ctx.d_grp, ctx.h_grp, sizeof(GroupState) * n_groups, cudaMemcpyHostToDevice, ctx.stream), "h2d");
     *ctx.h_ctl = Ctl{};
-    ctx.h_ctl->pending.v = (ex.roots ? n : 0) + int(ex.seeded.size());
-    ctx.h_ctl->tail.v = ex.seeded.size();
+    ctx.h_ctl->pending.v = (ex.roots ? n : 0) + int(n_seeded);
+    ctx.h_ctl->tail.v = n_seeded;
     ctx.h_ctl->live.v = n;
     ck(cudaMemcpyAsync(ctx.d_ctl, ctx.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx.stream), "h2d");
     if (wide)
@@ -411,7 +414,15 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
            "h2d seeded tasks");
         ck(cudaStreamSynchronize(ctx.stream), "h2d seeded tasks");  // `staged` is pageable
     }
-    f.seeded = ex.seeded.size();
+    if (!ex.wseeded.empty()) {
+        std::vector<WideSlot> staged(ex.wseeded);
+        for (size_t i = 0; i < staged.size(); ++i) staged[i].seq = i + 1;
+        ck(cudaMemcpyAsync(ctx.d_wslots, staged.data(), sizeof(WideSlot) * staged.size(),
+                           cudaMemcpyHostToDevice, ctx.stream),
+           "h2d seeded tasks");
+        ck(cudaStreamSynchronize(ctx.stream), "h2d seeded tasks");
+    }
+    f.seeded = n_seeded;
     *ctx.h_cancel = 0;
 
     KernelParams p{};
@@ -479,7 +490,8 @@ LaunchOut finish(InFlight& f) {
     out.smem_per_cta = kernel_smem_per_warp(f.bits, f.directed, f.smem_classes) * kWarpsPerCta;
     out.smem_classes = f.smem_classes;
     out.h2d_bytes = ((f.bits > 64 ? sizeof(WideDesc) : sizeof(InstanceDesc)) + sizeof(InstanceState)) * uint64_t(n) +
-                    sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl) + sizeof(TaskSlot) * f.seeded;
+                    sizeof(GroupState) * uint64_t(n_groups) + sizeof(Ctl) +
+                    (f.bits > 64 ? sizeof(WideSlot) : sizeof(TaskSlot)) * f.seeded;
     out.d2h_bytes = sizeof(InstanceState) * uint64_t(n) + sizeof(GroupState) * uint64_t(n_groups) +
                     sizeof(Counters) + sizeof(Ctl);
     out.launches = 2;  // ring reset + search kernel
@@ -544,6 +556,7 @@ struct DevicePlan {
     int device = 0;
     std::vector<Job> jobs;
     std::vector<TaskSlot> seeded;
+    std::vector<WideSlot> wseeded;
     bool roots = true;
 };
 
@@ -585,6 +598,7 @@ std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_o
     for (int i = 0; i < D; ++i) {
         LaunchExtras ex;
         ex.seeded = plans[i].seeded;
+        ex.wseeded = plans[i].wseeded;
         ex.roots = plans[i].roots;
         ex.relabeled = true;
         ex.peer_done_on_complete = peer_done_on_complete;
@@ -612,12 +626,17 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
     job.floor_size = o.floor_size;
     job.group = 0;
     relabel_for_throughput(job, o.seed);
-    if (std::max(job.g.n, job.h.n) > kMaxN)
-        throw Error("sharding one instance over devices needs n <= 64 (wide graphs run on one device)");
-    InstanceDesc desc;
-    pack_instance(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, &desc);
     const int per_dev = o.frontier > 0 ? o.frontier : 256;
-    Frontier fr = expand_frontier(desc, job.g.directed, per_dev * D, 0);
+    Frontier fr;
+    if (std::max(job.g.n, job.h.n) > kMaxN) {
+        auto desc = std::make_unique<WideDesc>();
+        pack_wide(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, desc.get());
+        fr = expand_frontier(*desc, job.g.directed, per_dev * D, 0);
+    } else {
+        InstanceDesc desc;
+        pack_instance(job.g, job.h, job.goal, o.disable_pruning == 0, job.floor_size, 0, &desc);
+        fr = expand_frontier(desc, job.g.directed, per_dev * D, 0);
+    }
     *host_nodes = fr.nodes;
     auto host_result = [&](bool optimal_by_host) {
         JobResult r;
@@ -631,7 +650,7 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
         r.nodes = fr.nodes;
         return r;
     };
-    if (fr.max_reached || fr.tasks.empty()) return host_result(true);  // the host already finished
+    if (fr.max_reached || (fr.tasks.empty() && fr.wtasks.empty())) return host_result(true);  // the host already finished
     std::vector<DevicePlan> plans(D);
     for (int i = 0; i < D; ++i) {
         plans[i].device = o.devices[i];
@@ -639,6 +658,7 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
         plans[i].roots = false;
     }
     for (size_t k = 0; k < fr.tasks.size(); ++k) plans[k % D].seeded.push_back(fr.tasks[k]);
+    for (size_t k = 0; k < fr.wtasks.size(); ++k) plans[k % D].wseeded.push_back(fr.wtasks[k]);
     std::vector<LaunchOut> outs = launch_multi(plans, o, false, fr.best_size, fr.best_v, fr.best_u);
     JobResult best = host_result(false);
     bool all_complete = true, any_done_max = false;

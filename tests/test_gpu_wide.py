@@ -129,3 +129,26 @@ def test_wide_orderings_parity():
         o = O.solve(go, ho, order=order)
         r = M.solve(g, h, M.SolveConfig(mode=M.MODE_PARITY, order=M.OrderingStrategy(order)))
         _same(r, o)
+
+
+@pytest.mark.parametrize("devices,frontier", [((0, 0), 0), ((0, 0, 0), 3)])
+def test_wide_sharded_over_devices(devices, frontier):
+    # one wide instance expanded on the host into wide frozen subtrees dealt to
+    # device contexts (repeated ordinals: the multi-GPU path on one B200)
+    for spec in RANDOM[:4]:
+        g, h = random_pair(*spec)
+        o = _oracle(g, h)
+        r = M.solve(g, h, M.SolveConfig(devices=devices, frontier=frontier))
+        assert r.status == M.SolveStatus.optimal and r.size == o.size, spec
+        assert M.verify(g, h, r.best)
+    g = complete(200)
+    r = M.solve(g, g, M.SolveConfig(devices=devices))
+    assert r.size == 200 and M.verify(g, g, r.best)
+
+
+def test_wide_multi_device_portfolio():
+    g, h = random_pair(100, 100, 0.5, False, 32)
+    o = _oracle(g, h)
+    pr = M.run_portfolio(g, h, ["recursive", "recursive+order=degree", "restarts:3"],
+                         M.SolveConfig(devices=(0, 0)))
+    assert pr.status == M.SolveStatus.optimal and pr.size == o.size and M.verify(g, h, pr.mapping)
