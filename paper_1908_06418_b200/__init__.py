@@ -40,7 +40,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmcsg.so")
+LIB_PATH = os.environ.get("MCSG_LIB", os.path.join(HERE, "libmcsg.so"))  # override: dev experiments
 MAX_N = 255
 
 __all__ = [
