@@ -238,6 +238,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             // task-level prune (engine_parallel.cpp:148-155): every child would prune
             if (bound <= prn_thr) skip = true;
         }
+        if (skip) {  // nothing of this task is entered (or counted)
+            cand = W{};
+            cont = 0;
+        }
 
         int cd = interval;     // nodes until the next poll
         unsigned splits = 0;   // flushed to s.st_splits at polls and at the task's end
@@ -372,6 +376,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             if (cnt >= 2)
                 for (int i = 0; i < (cnt + 1) / 2; ++i) give = set_drop_lowest(give);  // upper half
             const W keep = set_andnot(fc, give);
+            // the donor counted these children (and the continuation) when it
+            // selected level f; the receiver counts them when it resumes
+            cd += set_popc(give) + fr_cont(fw);
             // producer ticket; a warp is (probably) already waiting on it.
             // The slot is free once the consumer of ticket pos - cap released
             // it; the ring is far larger than the warp count, so this wait is
@@ -427,25 +434,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             return true;
         };
 
-// one counted search node (search_core.hpp:130), with the periodic poll
-#define MCSG_COUNT_NODE()                       \
-    if (--cd == 0) {                            \
-        if (lane == 0) {                        \
-            s.polled += unsigned(interval);     \
-            s.st_splits += splits;              \
-        }                                       \
-        splits = 0;                             \
-        cd = interval;                          \
-        if (!poll()) goto finish;               \
+// Node counting (search_core.hpp:130). Nodes are counted in bulk when a level
+// is selected: its |R*| children and its continuation are all counted nodes
+// (each is entered, even when its bound prunes it at once), so the u loop
+// carries no per-child counter. What a stop leaves unentered is subtracted at
+// the task's end; a donation hands its share of the count to the receiver.
+// The periodic poll runs when the countdown crosses zero.
+#define MCSG_COUNT_NODES(k)                                                     \
+    cd -= (k);                                                                 \
+    if (cd <= 0) {                                                             \
+        if (lane == 0) {                                                       \
+            s.polled += (unsigned long long)(long long)(interval - cd);        \
+            s.st_splits += splits;                                             \
+        }                                                                      \
+        splits = 0;                                                            \
+        cd = interval;                                                         \
+        if (!poll()) goto finish;                                              \
     }
 
         if (!skip) {
             if (!at_next) {
                 // the root node (search_core.hpp:129-166)
-                MCSG_COUNT_NODE();
+                MCSG_COUNT_NODES(1);
                 if (bound <= prn_thr) goto pop;
                 goto select;
             }
+            // a donated subtree: its remaining children and continuation
+            cd -= set_popc(cand) + cont;
             goto next;
 
         select:
@@ -461,33 +476,36 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             }
             x.prep_v(v, sel);
             cont = 1;
+            MCSG_COUNT_NODES(set_popc(cand) + 1);  // the children and the continuation
+            // Incumbent offer at the entry of the level's first child
+            // (search_core.hpp:145-155). Only a first child can improve: once
+            // it is entered the threshold is >= d+1 for its siblings, for
+            // later selects at this depth and after every pop back here.
+            if (d + 1 > off_thr) {
+                const int u = set_ctz(cand);
+                offer(d, u);
+                raise_best(d + 1);
+                const bool goal_hit = goal > 0 && d + 1 >= goal;                 // search_core.hpp:147-150
+                const bool max_hit = prune && goal == 0 && d + 1 >= maxp;        // search_core.hpp:151-154
+                if (goal_hit || max_hit) {
+                    if (lane == 0) {
+                        if (goal_hit) gs->reached = 1;
+                        if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
+                    }
+                    if (grp == 0 && lane < p.n_peers) {  // stop every device
+                        if (goal_hit) atomicExch_system(&p.peer_grp[lane]->reached, 1);
+                        atomicExch_system(&p.peer_grp[lane]->done, 1u);
+                    }
+                    cand = set_drop_lowest(cand);  // u was entered; the rest never is
+                    goto finish;
+                }
+            }
 
         next:
             // ---- u loop (search_core.hpp:183-200): children in ascending u
             while (set_any(cand)) {
-                const int u = set_ctz(cand);
+                const int u = set_ctz(cand);  // the child's entry (counted at select)
                 cand = set_drop_lowest(cand);
-                MCSG_COUNT_NODE();  // the child's entry
-                if (d + 1 > off_thr) {
-                    offer(d, u);
-                    raise_best(d + 1);
-                    if (goal > 0 && d + 1 >= goal) {  // search_core.hpp:147-150
-                        if (lane == 0) {
-                            gs->reached = 1;
-                            if (atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
-                        }
-                        if (grp == 0 && lane < p.n_peers) {  // stop every device
-                            atomicExch_system(&p.peer_grp[lane]->reached, 1);
-                            atomicExch_system(&p.peer_grp[lane]->done, 1u);
-                        }
-                        goto finish;
-                    }
-                    if (prune && goal == 0 && d + 1 >= maxp) {  // search_core.hpp:151-154
-                        if (lane == 0 && atomicCAS(&gs->done, 0u, 1u) == 0u) gs->winner = inst;
-                        if (grp == 0 && lane < p.n_peers) atomicExch_system(&p.peer_grp[lane]->done, 1u);
-                        goto finish;
-                    }
-                }
                 typename X::HParts h;
                 x.h_parts(u, h);
                 const int cbound = d + 1 + int(x.child_sum(u, h));
@@ -495,9 +513,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 // ---- materialise the child (filter_classes) one level up
                 int cb = base + nc;
                 const int need = min(nc * P, NB);
-                if (cb < x.cap && cb + need > x.cap) {
-                    cb = x.cap;
-                    if (lane == 0) s.st_spills += 1;
+                if constexpr (X::kSpill) {
+                    // a level never straddles shared memory and the HBM spill area
+                    if (cb < x.cap && cb + need > x.cap) {
+                        cb = x.cap;
+                        if (lane == 0) s.st_spills += 1;
+                    }
                 }
                 if (cb + need > stack_limit) {  // cannot happen with the host's sizing
                     if (lane == 0) {
@@ -525,8 +546,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 goto select;
             }
             // ---- v left unmatched (search_core.hpp:201-212): a counted node
-            if (cont) {
-                MCSG_COUNT_NODE();
+            if (cont) {  // (counted at select)
                 x.cont_step(sel, v, nc, base, bound);
                 __syncwarp();
                 cont = 0;
@@ -553,15 +573,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             x.prep_v(v, sel);
             goto next;
         }
-#undef MCSG_COUNT_NODE
+#undef MCSG_COUNT_NODES
     finish : {
         {
             const long long t = clock64();
             if (lane == 0) s.st_busy += (unsigned long long)(t - t_mark);
             t_mark = t;
         }
+        {
+            // nodes counted at select but never entered (a stop, or levels
+            // abandoned by an abort): the open levels' remaining children
+            // and continuations, plus the current level's
+            int left = 0;
+            for (int lv = root + lane; lv < d; lv += 32) left += set_popc(s.f_cand[lv]) + fr_cont(s.f_word[lv]);
+            cd += int(__reduce_add_sync(kFull, unsigned(left))) + set_popc(cand) + cont;
+        }
         if (lane == 0) {
-            const unsigned long long task_nodes = s.polled + unsigned(interval - cd);
+            const unsigned long long task_nodes = s.polled + (unsigned long long)(long long)(interval - cd);
             s.st_nodes += task_nodes;
             s.st_splits += splits;
             if (task_nodes) atomicAdd(&is->nodes, task_nodes);

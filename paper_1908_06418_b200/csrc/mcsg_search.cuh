@@ -586,6 +586,7 @@ struct WideSearch {
     static constexpr int NB = Sm::NB;
     static constexpr int P = DIR ? 4 : 2;
     static constexpr int kMinBlocks = 2;
+    static constexpr bool kSpill = true;
     struct HParts {
         Set o, i;  // H rows of u (out; in when directed)
     };
