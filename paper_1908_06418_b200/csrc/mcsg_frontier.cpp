@@ -33,6 +33,11 @@ inline int ctz(const HSet& x) {
         if (x[i]) return 64 * i + __builtin_ctzll(x[i]);
     return -1;
 }
+inline int top(const HSet& x) {
+    for (int i = kWideWords - 1; i >= 0; --i)
+        if (x[i]) return 64 * i + 63 - __builtin_clzll(x[i]);
+    return -1;
+}
 inline bool any(const HSet& x) { return (x[0] | x[1] | x[2] | x[3]) != 0; }
 inline HSet band(const HSet& a, const HSet& b) { return {a[0] & b[0], a[1] & b[1], a[2] & b[2], a[3] & b[3]}; }
 inline HSet bnot(const HSet& a) { return {~a[0], ~a[1], ~a[2], ~a[3]}; }
@@ -65,23 +70,22 @@ int bound_of(const Node& n) {
 }
 
 // select_label_class + select_vertex (label_classes.cpp:47-78) on a node that
-// survived its prune test; false when no class remains. The class order is
-// the kernel's key order: (max(|L|,|R|), min, lowest left id, slot).
+// survived its prune test; false when no class remains. Same rule as the
+// throughput kernel: G is relabelled in REVERSE select_vertex order, so the
+// class order is (max(|L|,|R|), min, highest left id, slot) and v is the
+// highest id of the class.
 template <class D>
 bool enter(Node n, const D& d, Branch* out) {
+    (void)d;
     std::tuple<int, int, int, int> best{1 << 30, 0, 0, 0};
     int sel = -1;
     for (int i = 0; i < int(n.cls.size()); ++i) {
         const int pl = popc(n.cls[i].first), pr = popc(n.cls[i].second);
-        const std::tuple<int, int, int, int> k{std::max(pl, pr), std::min(pl, pr), ctz(n.cls[i].first), i};
+        const std::tuple<int, int, int, int> k{std::max(pl, pr), std::min(pl, pr), -top(n.cls[i].first), i};
         if (k < best) best = k, sel = i;
     }
     if (sel < 0) return false;
-    HSet l = n.cls[sel].first;
-    uint32_t vk = ~0u;
-    int v = -1;
-    for (int x = ctz(l); x >= 0; l = without(l, x), x = ctz(l))
-        if (uint32_t(d.vkey[x]) < vk) vk = uint32_t(d.vkey[x]), v = x;
+    const int v = top(n.cls[sel].first);
     out->v = v;
     out->sel = sel;
     out->cand = n.cls[sel].second;

@@ -232,8 +232,10 @@ Job make_job(const HostGraph& g, const HostGraph& h, int order) {
 }
 
 // Throughput mode: relabel G so that its ids follow select_vertex's order
-// (degree desc, id asc; label_classes.cpp:69-78). The kernel then picks v with
-// one ctz; the composed permutation is undone on the returned mapping.
+// (degree desc, id asc; label_classes.cpp:69-78) REVERSED: the first vertex
+// of that order gets the highest id. The kernel then picks v with one FLO
+// (highest set bit); the composed permutation is undone on the returned
+// mapping.
 //
 // A nonzero seed is the GPU counterpart of the "restarts:<seed>" portfolio
 // member (restarts.cpp:213-228 draws the next segment with mt19937_64): it
@@ -252,7 +254,7 @@ void relabel_for_throughput(Job& j, uint64_t seed = 0) {
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return deg[a] != deg[b] ? deg[a] > deg[b] : tie[a] < tie[b]; });
     std::vector<int> fwd(n);
-    for (int pos = 0; pos < n; ++pos) fwd[order[pos]] = pos;
+    for (int pos = 0; pos < n; ++pos) fwd[order[pos]] = n - 1 - pos;
     std::vector<int> inv(n);
     for (int v = 0; v < n; ++v) inv[fwd[v]] = j.inv_g.empty() ? v : j.inv_g[v];
     j.g = j.g.permuted(fwd);

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             d = root = 0;
             x.load_level(0, nc);
             unsigned sm;
-            key = x.scan_key(nc, &sm);
+            key = x.template scan_key<!PAR>(nc, &sm);
             have_key = true;
             bound = int(sm);
         } else {
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
         }
 
         int cd = interval;     // nodes until the next poll
+        int lim = 0;           // u loop: prune threshold minus |M|+1
         unsigned splits = 0;   // flushed to s.st_splits at polls and at the task's end
         bool abort_all = false;
 
@@ -372,10 +373,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             const W fc = s.f_cand[f];
             const unsigned long long fw = s.f_word[f];
             const int cnt = set_popc(fc);
-            W give = fc;
+            // hand over the half the donor would reach last (throughput mode
+            // walks u from the top: the lower half)
+            W keep = fc;
             if (cnt >= 2)
-                for (int i = 0; i < (cnt + 1) / 2; ++i) give = set_drop_lowest(give);  // upper half
-            const W keep = set_andnot(fc, give);
+                for (int i = 0; i < cnt / 2; ++i) keep = set_drop_lowest(keep);
+            else
+                keep = W{};
+            const W give = set_andnot(fc, keep);
             // the donor counted these children (and the continuation) when it
             // selected level f; the receiver counts them when it resumes
             cd += set_popc(give) + fr_cont(fw);
@@ -465,13 +470,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
 
         select:
             // ---- the node survived its prune test: choose class and vertex
-            if (!have_key) key = x.scan_key(nc, nullptr);
+            if (!have_key) key = x.template scan_key<!PAR>(nc, nullptr);
             if (key == kNoKey) goto pop;
             sel = X::key_slot(key);
             {
                 const W lsel = x.class_l(sel);
                 if constexpr (PAR) v = x.select_vertex(lsel);
-                else v = set_ctz(lsel);  // G is relabelled in select_vertex order
+                else v = set_top(lsel);  // G is relabelled in reverse select_vertex order
                 cand = x.class_r(sel);
             }
             x.prep_v(v, sel);
@@ -482,7 +487,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             // it is entered the threshold is >= d+1 for its siblings, for
             // later selects at this depth and after every pop back here.
             if (d + 1 > off_thr) {
-                const int u = set_ctz(cand);
+                const int u = PAR ? set_ctz(cand) : set_top(cand);
                 offer(d, u);
                 raise_best(d + 1);
                 const bool goal_hit = goal > 0 && d + 1 >= goal;                 // search_core.hpp:147-150
@@ -496,20 +501,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                         if (goal_hit) atomicExch_system(&p.peer_grp[lane]->reached, 1);
                         atomicExch_system(&p.peer_grp[lane]->done, 1u);
                     }
-                    cand = set_drop_lowest(cand);  // u was entered; the rest never is
+                    cand = set_without(cand, u);  // u was entered; the rest never is
                     goto finish;
                 }
             }
 
         next:
             // ---- u loop (search_core.hpp:183-200): children in ascending u
+            // Parity mode walks u in ascending id (the reference's order);
+            // throughput mode from the top (one FLO instead of BREV + FLO).
+            lim = prn_thr - (d + 1);  // a child survives when its class sum exceeds lim
             while (set_any(cand)) {
-                const int u = set_ctz(cand);  // the child's entry (counted at select)
-                cand = set_drop_lowest(cand);
+                const int u = PAR ? set_ctz(cand) : set_top(cand);  // the child's entry (counted at select)
+                cand = set_without(cand, u);
                 typename X::HParts h;
                 x.h_parts(u, h);
-                const int cbound = d + 1 + int(x.child_sum(u, h));
-                if (cbound <= prn_thr) continue;  // pruned at entry
+                const int csum = int(x.child_sum(u, h));
+                if (csum <= lim) continue;  // pruned at entry
+                const int cbound = d + 1 + csum;
                 // ---- materialise the child (filter_classes) one level up
                 int cb = base + nc;
                 const int need = min(nc * P, NB);
@@ -533,7 +542,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                     s.f_word[d] = pack_frame(base, nc, sel, v, bound, cont, u);
                 }
                 unsigned ckey;
-                const int cnc = x.split(u, v, h, cb, &ckey);
+                const int cnc = x.template split<!PAR>(u, v, h, cb, &ckey);
                 __syncwarp();
                 ++splits;
                 ++d;

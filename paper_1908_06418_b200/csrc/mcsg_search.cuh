@@ -75,6 +75,11 @@ template <typename W>
 __device__ __forceinline__ W set_drop_lowest(W x) { return x & (x - 1); }
 template <typename W>
 __device__ __forceinline__ W set_andnot(W a, W b) { return a & ~b; }
+// highest set bit (-1 when empty): one FLO, where the lowest costs BREV + FLO
+__device__ __forceinline__ int set_top(uint32_t x) { return 31 - __clz(x); }
+__device__ __forceinline__ int set_top(uint64_t x) { return 63 - __clzll(x); }
+template <typename W>
+__device__ __forceinline__ W set_without(W x, int b) { return x & ~(W(1) << b); }
 
 template <int NW>
 __device__ __forceinline__ bool set_any(const WSet<NW>& x) {
@@ -97,6 +102,14 @@ __device__ __forceinline__ int set_ctz(const WSet<NW>& x) {
 #pragma unroll
     for (int i = NW - 1; i >= 0; --i)
         if (x.w[i]) r = 64 * i + __ffsll(x.w[i]) - 1;
+    return r;
+}
+template <int NW>
+__device__ __forceinline__ int set_top(const WSet<NW>& x) {
+    int r = -1;
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+        if (x.w[i]) r = 64 * i + 63 - __clzll(x.w[i]);
     return r;
 }
 template <int NW>
@@ -131,6 +144,10 @@ __device__ __forceinline__ WSet<NW> set_bit(int v) {
 #pragma unroll
     for (int i = 0; i < NW; ++i) r.w[i] = (v >> 6) == i ? (1ull << (v & 63)) : 0ull;
     return r;
+}
+template <int NW>
+__device__ __forceinline__ WSet<NW> set_without(const WSet<NW>& x, int b) {
+    return set_andnot(x, set_bit<NW>(b));
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -180,10 +197,14 @@ __device__ __forceinline__ unsigned ld_volatile_u(const uint32_t* p) {
 
 // select_label_class key (label_classes.cpp:47-67): min over classes of
 // (max(|L|,|R|), min(|L|,|R|), lowest left id); low 7 bits carry the slot.
-template <typename W>
+// TOP (throughput mode): the host relabels G in REVERSE select_vertex order,
+// so "lowest left id" there is "highest left id" here: the tie field is the
+// count of leading zeros (one FLO), and the min still picks that class.
+template <typename W, bool TOP = false>
 __device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
     const unsigned mx = max(pl, pr), mn = min(pl, pr);
-    return (mx << 20) | (mn << 13) | (unsigned(Bits<W>::ctz(l)) << 7) | unsigned(slot);
+    const int tie = TOP ? Bits<W>::n - 1 - set_top(l) : Bits<W>::ctz(l);
+    return (mx << 20) | (mn << 13) | (unsigned(tie) << 7) | unsigned(slot);
 }
 
 // Packed DFS frame (one per search level): where the level's classes are,
@@ -356,6 +377,7 @@ struct Search {
     }
 
     // compute_bound + select_label_class over the register-resident level
+    template <bool TOP>
     __device__ __forceinline__ unsigned scan_key(int nc, unsigned* sum) const {
         unsigned key = kNoKey, sm = 0;
 #pragma unroll
@@ -364,7 +386,7 @@ struct Search {
             if (c < nc) {
                 const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
                 sm += unsigned(min(pl, pr));
-                key = min(key, class_key<W>(pl, pr, L[k], c));
+                key = min(key, class_key<W, TOP>(pl, pr, L[k], c));
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -484,11 +506,13 @@ struct Search {
     // filter_classes (label_classes.cpp:80-108): split every class by the
     // codes toward (v,u), drop one-sided parts, compact into the next level
     // with ballots; returns the child's class count and its best class key.
+    template <bool TOP>
     __device__ __forceinline__ int split(int u, int v, const HParts& hp, int cbase, unsigned* key_out) {
-        if (in_smem(cbase)) return split_into(u, v, hp.h, scls + cbase, key_out);
-        return split_into(u, v, hp.h, gcls + (cbase - cap), key_out);
+        if (in_smem(cbase)) return split_into<TOP>(u, v, hp.h, scls + cbase, key_out);
+        return split_into<TOP>(u, v, hp.h, gcls + (cbase - cap), key_out);
     }
 
+    template <bool TOP>
     __device__ __forceinline__ int split_into(int u, int v, const W h[P], Cls<W>* q, unsigned* key_out) {
         W g[P];
         g_parts(v, g);
@@ -507,7 +531,7 @@ struct Search {
                 if (keep) {
                     const int pos = total + __popc(m & lt);
                     q[pos] = Cls<W>{lp, rp};
-                    key = min(key, class_key<W>(lc[k][pp], Bits<W>::popc(rp), lp, pos));
+                    key = min(key, class_key<W, TOP>(lc[k][pp], Bits<W>::popc(rp), lp, pos));
                 }
                 total += __popc(m);
             }
@@ -610,9 +634,10 @@ struct WideSearch {
     __device__ static __forceinline__ int key_slot(unsigned key) { return int(key & 255u); }
 
     // select_label_class key: (max, min, lowest left id, slot), 8 bits each
+    template <bool TOP>
     __device__ static __forceinline__ unsigned class_key(int pl, int pr, const Set& l, int slot) {
         const unsigned mx = max(pl, pr), mn = min(pl, pr);
-        return (mx << 24) | (mn << 16) | (unsigned(set_ctz(l)) << 8) | unsigned(slot);
+        return (mx << 24) | (mn << 16) | (unsigned(TOP ? 255 - set_top(l) : set_ctz(l)) << 8) | unsigned(slot);
     }
 
     __device__ static __forceinline__ Set row(const uint64_t (*rows)[kWideWords], int v) {
@@ -691,6 +716,7 @@ struct WideSearch {
     }
 
     // compute_bound + select_label_class over the level
+    template <bool TOP>
     __device__ __forceinline__ unsigned scan_key(int nc, unsigned* sum) const {
         unsigned key = kNoKey, sm = 0;
         for (int c0 = 0; c0 < nc; c0 += 32) {
@@ -699,7 +725,7 @@ struct WideSearch {
                 const C x = lvl[c];
                 const int pl = set_popc(x.l), pr = set_popc(x.r);
                 sm += unsigned(min(pl, pr));
-                key = min(key, class_key(pl, pr, x.l, c));
+                key = min(key, class_key<TOP>(pl, pr, x.l, c));
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -778,6 +804,7 @@ struct WideSearch {
     }
 
     // filter_classes (label_classes.cpp:80-108) into the next level at cbase
+    template <bool TOP>
     __device__ __forceinline__ int split(int u, int v, const HParts& h, int cbase, unsigned* key_out) {
         (void)v;
         C* q = at(cbase);
@@ -797,7 +824,7 @@ struct WideSearch {
                 if (keep) {
                     const int pos = total + __popc(m & lt);
                     q[pos] = C{lp, rp};
-                    key = min(key, class_key(set_popc(lp), set_popc(rp), lp, pos));
+                    key = min(key, class_key<TOP>(set_popc(lp), set_popc(rp), lp, pos));
                 }
                 total += __popc(m);
             }
