@@ -89,7 +89,8 @@ bool enter(Node n, const D& d, Branch* out) {
     out->v = v;
     out->sel = sel;
     out->cand = n.cls[sel].second;
-    out->cont = 1;
+    // the kernel's continuation byte: owned | [|L*| <= |R*|] (kContDec)
+    out->cont = 1 | (popc(n.cls[sel].first) <= popc(n.cls[sel].second) ? 2 : 0);
     out->node = std::move(n);
     return true;
 }

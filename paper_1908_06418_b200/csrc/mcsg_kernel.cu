@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             const W give = set_andnot(fc, keep);
             // the donor counted these children (and the continuation) when it
             // selected level f; the receiver counts them when it resumes
-            cd += set_popc(give) + fr_cont(fw);
+            cd += set_popc(give) + (fr_cont(fw) != 0);
             // producer ticket; a warp is (probably) already waiting on it.
             // The slot is free once the consumer of ticket pos - cap released
             // it; the ring is far larger than the warp count, so this wait is
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 X::put_cand(*sl, h, give);
                 sl->hdr = h;
                 s.f_cand[f] = keep;
-                s.f_word[f] = fw & ~kFrameCont;  // the continuation left with the task
+                s.f_word[f] = fw & ~kFrameContByte;  // the continuation left with the task
             }
             fence_acq_rel_gpu();  // payload before the release of the slot
             __syncwarp();
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 goto select;
             }
             // a donated subtree: its remaining children and continuation
-            cd -= set_popc(cand) + cont;
+            cd -= set_popc(cand) + (cont != 0);
             goto next;
 
         select:
@@ -478,9 +478,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 if constexpr (PAR) v = x.select_vertex(lsel);
                 else v = set_top(lsel);  // G is relabelled in reverse select_vertex order
                 cand = x.class_r(sel);
+                cont = kContOwned | (set_popc(lsel) <= set_popc(cand) ? kContDec : 0);
             }
             x.prep_v(v, sel);
-            cont = 1;
             MCSG_COUNT_NODES(set_popc(cand) + 1);  // the children and the continuation
             // Incumbent offer at the entry of the level's first child
             // (search_core.hpp:145-155). Only a first child can improve: once
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             }
             // ---- v left unmatched (search_core.hpp:201-212): a counted node
             if (cont) {  // (counted at select)
-                x.cont_step(sel, v, nc, base, bound);
+                x.cont_step(sel, cont, base, bound);
                 __syncwarp();
                 cont = 0;
                 have_key = false;
@@ -594,8 +594,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             // abandoned by an abort): the open levels' remaining children
             // and continuations, plus the current level's
             int left = 0;
-            for (int lv = root + lane; lv < d; lv += 32) left += set_popc(s.f_cand[lv]) + fr_cont(s.f_word[lv]);
-            cd += int(__reduce_add_sync(kFull, unsigned(left))) + set_popc(cand) + cont;
+            for (int lv = root + lane; lv < d; lv += 32) left += set_popc(s.f_cand[lv]) + (fr_cont(s.f_word[lv]) != 0);
+            cd += int(__reduce_add_sync(kFull, unsigned(left))) + set_popc(cand) + (cont != 0);
         }
         if (lane == 0) {
             const unsigned long long task_nodes = s.polled + (unsigned long long)(long long)(interval - cd);

@@ -213,7 +213,11 @@ __device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
 // Byte-aligned fields: packing is a chain of IMADs, unpacking byte extracts.
 //   low word : base (16 bits) | nc << 16 | sel << 24
 //   high word: v | bound << 8 | cont << 16 | u << 24
-constexpr unsigned long long kFrameCont = 1ull << 48;
+// The continuation byte: 0 when the "v unmatched" continuation no longer
+// belongs to the level, else kContOwned | (kContDec when |L*| <= |R*|, i.e.
+// when the continuation lowers the bound by one).
+constexpr int kContOwned = 1, kContDec = 2;
+constexpr unsigned long long kFrameContByte = 0xffull << 48;
 __device__ __forceinline__ unsigned long long pack_frame(int base, int nc, int sel, int v, int bound,
                                                          int cont, int u) {
     const unsigned lo = unsigned(base) + (unsigned(nc) << 16) + (unsigned(sel) << 24);
@@ -386,7 +390,7 @@ struct Search {
             if (c < nc) {
                 const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
                 sm += unsigned(min(pl, pr));
-                key = min(key, class_key<W, TOP>(pl, pr, L[k], c));
+                if (pl) key = min(key, class_key<W, TOP>(pl, pr, L[k], c));  // L = {}: a dead class
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -541,35 +545,20 @@ struct Search {
     }
 
     // "v unmatched" (search_core.hpp:201-212): the bound drops by
-    // [|L*| <= |R*|], v leaves L* and an emptied class is dropped (the last
-    // class takes its slot), in registers and in the level's stack copy.
-    __device__ __forceinline__ void cont_step(int sel, int v, int& nc, int base, int& bound) {
-        const W lsel = class_l(sel), rsel = class_r(sel);
-        bound -= (Bits<W>::popc(lsel) <= Bits<W>::popc(rsel)) ? 1 : 0;
-        const W nl = lsel & ~(W(1) << v);
+    // [|L*| <= |R*|] (decided at select: kContDec) and v leaves L*. The lane
+    // owning class sel already holds L* \ {v} (LX, prep_v) and writes it to
+    // the level's stack copy. A class emptied this way stays in its slot,
+    // dead: it adds 0 to every bound and is never selected (scan_key), which
+    // is what dropping it does (label_classes.cpp:95-105).
+    __device__ __forceinline__ void cont_step(int sel, int cbits, int base, int& bound) {
+        bound -= (cbits & kContDec) ? 1 : 0;
         Cls<W>* lvl = at(base);
-        if (nl != 0) {
 #pragma unroll
-            for (int k = 0; k < S; ++k)
-                if (lane + 32 * k == sel) L[k] = nl;
-            if (lane == 0) lvl[sel].l = nl;
-        } else {
-            const W ll = class_l(nc - 1), lr = class_r(nc - 1);
-#pragma unroll
-            for (int k = 0; k < S; ++k) {
-                const int c = lane + 32 * k;
-                if (c == nc - 1) {  // lanes past the level must hold empty classes
-                    L[k] = 0;
-                    R[k] = 0;
-                }
-                if (c == sel && sel != nc - 1) {
-                    L[k] = ll;
-                    R[k] = lr;
-                }
+        for (int k = 0; k < S; ++k)
+            if (lane + 32 * k == sel) {
+                L[k] = LX[k];
+                lvl[sel].l = LX[k];
             }
-            if (lane == 0 && sel != nc - 1) lvl[sel] = Cls<W>{ll, lr};
-            --nc;
-        }
     }
 };
 
@@ -725,7 +714,7 @@ struct WideSearch {
                 const C x = lvl[c];
                 const int pl = set_popc(x.l), pr = set_popc(x.r);
                 sm += unsigned(min(pl, pr));
-                key = min(key, class_key<TOP>(pl, pr, x.l, c));
+                if (pl) key = min(key, class_key<TOP>(pl, pr, x.l, c));  // L = {}: a dead class
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -833,21 +822,12 @@ struct WideSearch {
         return total;
     }
 
-    // "v unmatched" (search_core.hpp:201-212), in the level's memory
-    __device__ __forceinline__ void cont_step(int sel, int v, int& nc, int base, int& bound) {
+    // "v unmatched" (search_core.hpp:201-212), in the level's memory (an
+    // emptied class stays in its slot, dead; see Search::cont_step)
+    __device__ __forceinline__ void cont_step(int sel, int cbits, int base, int& bound) {
         (void)base;
-        const C cs = lvl[sel], last = lvl[nc - 1];
-        __syncwarp();  // every lane has read the level before lane 0 rewrites it
-        bound -= (set_popc(cs.l) <= set_popc(cs.r)) ? 1 : 0;
-        const Set nl = set_andnot(cs.l, set_bit<NW>(v));
-        if (set_any(nl)) {
-            if (lane == 0) lvl[sel].l = nl;
-        } else {
-            if (lane == 0 && sel != nc - 1) lvl[sel] = last;
-            --nc;
-        }
-        __syncwarp();
-        lnc = nc;
+        bound -= (cbits & kContDec) ? 1 : 0;
+        if (lane == 0) lvl[sel].l = set_andnot(lvl[sel].l, vb);
     }
 };
 
