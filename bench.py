@@ -309,12 +309,19 @@ def run_ours(args, rank, world, local_rank):
     clk_mhz = float(peaks.get("sm_max_mhz") or 1965.0)
     peak_issue = sms * 4 * clk_mhz * 1e6  # warp-instructions / s (4 schedulers per SM)
     inst_per_node = prof.get("warp_inst_per_node")
+    import hashlib
+    sha = hashlib.sha1()
+    for f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_device.h"):
+        with open(os.path.join(ROOT, "paper_1908_06418_b200", "csrc", f), "rb") as fh:
+            sha.update(fh.read())
+    profile_current = prof.get("kernel_src_sha1") == sha.hexdigest()
     roofline = {
         "bound": "issue",
         "achieved": (value / world) * inst_per_node if inst_per_node else None,
         "peak": peak_issue, "unit": "warp-inst/s",
         "frac": ((value / world) * inst_per_node / peak_issue) if inst_per_node else None,
         "traffic": prof.get("dram_bytes_per_launch"),
+        "profile_matches_kernel": profile_current,  # False: profiles/ is from other kernel sources
         "basis": (f"issue roof = {sms} SMs x 4 schedulers x {clk_mhz:g} MHz (sm_max_mhz, "
                   f"MEASURED_PEAKS.json); per-node cost {inst_per_node} warp-instructions from "
                   f"profiles/ncu_summary.json; neither HBM nor tensor cores bind (SURVEY 8(d))"),

@@ -28,4 +28,11 @@ out['nodes_per_launch'] = nodes
 out['stall_pct'] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0)) if v}
 out['pipes_pct'] = {k.replace('sm__inst_executed_pipe_', '').replace('.avg.pct_of_peak_sustained_active', ''): v
                     for k, v in sorted(pipes.items(), key=lambda x: -(x[1] or 0)) if v}
+# the kernel sources the profile belongs to (bench.py flags a stale profile)
+import hashlib, os
+_h = hashlib.sha1()
+_root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1908_06418_b200", "csrc")
+for _f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_device.h"):
+    _h.update(open(os.path.join(_root, _f), "rb").read())
+out['kernel_src_sha1'] = _h.hexdigest()
 print(json.dumps(out, indent=1))
