@@ -537,10 +537,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                     abort_all = true;
                     goto finish;
                 }
-                if (lane == 0) {
-                    s.f_cand[d] = cand;
-                    s.f_word[d] = pack_frame(base, nc, sel, v, bound, cont, u);
-                }
+                // every lane stores the same (uniform) frame: no branch
+                s.f_cand[d] = cand;
+                s.f_word[d] = pack_frame(base, nc, sel, v, bound, cont, u);
                 unsigned ckey;
                 const int cnc = x.template split<!PAR>(u, v, h, cb, &ckey);
                 __syncwarp();

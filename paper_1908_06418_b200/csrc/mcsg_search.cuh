@@ -199,12 +199,14 @@ __device__ __forceinline__ unsigned ld_volatile_u(const uint32_t* p) {
 // (max(|L|,|R|), min(|L|,|R|), lowest left id); low 7 bits carry the slot.
 // TOP (throughput mode): the host relabels G in REVERSE select_vertex order,
 // so "lowest left id" there is "highest left id" here: the tie field is the
-// count of leading zeros (one FLO), and the min still picks that class.
+// highest id flipped within its 6-bit field, and the min still picks that
+// class. The fields are packed with multiply-adds (mx < 128, mn < 128,
+// tie < 64, slot < 128).
 template <typename W, bool TOP = false>
 __device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
     const unsigned mx = max(pl, pr), mn = min(pl, pr);
-    const int tie = TOP ? Bits<W>::n - 1 - set_top(l) : Bits<W>::ctz(l);
-    return (mx << 20) | (mn << 13) | (unsigned(tie) << 7) | unsigned(slot);
+    const unsigned tie = TOP ? unsigned(set_top(l)) ^ 63u : unsigned(Bits<W>::ctz(l));
+    return ((mx * 128u + mn) * 64u + tie) * 128u + unsigned(slot);
 }
 
 // Packed DFS frame (one per search level): where the level's classes are,
