@@ -143,6 +143,9 @@ struct Counters {
     unsigned long long spills;       // levels placed in the HBM spill area
     unsigned long long t_start_ns;   // min %globaltimer over warps at kernel start
     unsigned long long overflow;     // class-stack overflow (must stay 0)
+    unsigned long long ring_stall;   // a producer waited > 2 s for a ring slot (must stay 0)
+    unsigned long long bad_task;     // a consumed subtree had an impossible header (must stay 0)
+    unsigned long long stall_pos, stall_head, stall_tail, stall_seq;  // its ticket and the ring state
     unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
     unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks
 };
@@ -176,6 +179,7 @@ struct KernelParams {
     WideSlot* wslots;           // wide kernels
     Ctl* ctl;
     uint32_t cap_mask;       // ring capacity - 1 (power of two)
+    unsigned long long ring_watchdog_ns;  // a producer waiting longer for a slot aborts the launch
     int32_t n_inst;
     int32_t n_roots;         // instances handed out as root tasks (0: the ring was pre-seeded)
     // Cross-device incumbent of group 0 (one instance sharded over devices, or

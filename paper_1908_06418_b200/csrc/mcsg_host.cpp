@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -435,7 +436,16 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.slots = ctx.d_slots;
     p.wslots = ctx.d_wslots;
     p.ctl = ctx.d_ctl;
-    p.cap_mask = ring_cap - 1;
+    // Debug hooks (tests only): a smaller ring and a shorter producer
+    // watchdog exercise the stall-abort path.
+    uint32_t cap = ring_cap;
+    if (const char* e = std::getenv("MCSG_DEBUG_RING_CAP")) {
+        const uint32_t c = uint32_t(std::strtoul(e, nullptr, 10));
+        if (c >= 1 && c <= ring_cap && (c & (c - 1)) == 0) cap = c;
+    }
+    p.cap_mask = cap - 1;
+    p.ring_watchdog_ns = 2000000000ull;
+    if (const char* e = std::getenv("MCSG_DEBUG_RING_WATCHDOG_NS")) p.ring_watchdog_ns = std::strtoull(e, nullptr, 10);
     p.n_inst = n;
     p.n_roots = ex.roots ? n : 0;
     p.n_peers = int(ex.peers.size());
@@ -498,6 +508,15 @@ LaunchOut finish(InFlight& f) {
                     sizeof(Counters) + sizeof(Ctl);
     out.launches = 2;  // ring reset + search kernel
     if (out.counters.overflow) throw Error("class stack overflow (internal error)");
+    if (out.counters.bad_task)
+        throw Error("malformed subtree in the task ring (internal error): ticket " +
+                    std::to_string(out.counters.stall_pos) + " inst " + std::to_string(out.counters.stall_head) +
+                    " depth<<8|nc " + std::to_string(out.counters.stall_tail) + " seq " +
+                    std::to_string(out.counters.stall_seq));
+    if (out.counters.ring_stall)
+        throw Error("task ring stalled (internal error): ticket " + std::to_string(out.counters.stall_pos) +
+                    " head " + std::to_string(out.counters.stall_head) + " tail " +
+                    std::to_string(out.counters.stall_tail) + " slot seq " + std::to_string(out.counters.stall_seq));
 
     const int stop = ctx.h_ctl->stop.v;
     for (int gi = 0; gi < n_groups; ++gi) {

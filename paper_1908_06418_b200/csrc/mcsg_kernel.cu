@@ -34,6 +34,8 @@ namespace mcsg {
 // while fewer than kStarvedQueue subtrees are queued, even when no warp is
 // waiting; warps that finish a task take queued subtrees in ticket order.
 constexpr int kStarvedQueue = 256;
+// Poll interval (nodes) while warps are waiting for work.
+constexpr int kFastPoll = 16;
 
 template <class X, bool PAR>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
@@ -147,6 +149,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             __syncwarp();
             hdr = slot->hdr;
             inst = hdr.inst;
+            // a malformed subtree means the ring protocol broke: stop the
+            // launch with an error instead of touching memory with it
+            if (unsigned(inst) >= unsigned(p.n_inst) || hdr.depth > NB || hdr.nc > NB || hdr.kind != kTaskBranch) {
+                if (lane == 0) {
+                    Counters* c = p.counters;
+                    if (atomicAdd(&c->bad_task, 1ull) == 0) {
+                        c->stall_pos = slot_pos;
+                        c->stall_head = (unsigned long long)(unsigned)inst;
+                        c->stall_tail = (unsigned long long)hdr.depth << 8 | hdr.nc;
+                        c->stall_seq = ld_relaxed(&slot->seq);
+                    }
+                    atomicCAS(&ctl->stop.v, 0, 3);
+                }
+                stop_all = true;
+                break;
+            }
         }
         if (inst != cur_inst) {
             const auto& dsc = X::descs(p)[inst];
@@ -243,7 +261,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             cont = 0;
         }
 
-        int cd = interval;     // nodes until the next poll
+        // nodes until the next poll (cd), counted from cd0; a throughput task
+        // polls early once, and every kFastPoll nodes while warps wait for work
+        // a root task polls early: a launch with few roots starts fanning out
+        // at once (donated subtrees keep the normal interval: polling them
+        // early too floods the ring with tiny tasks)
+        int cd0 = (!PAR && !branch) ? kFastPoll : interval;
+        int cd = cd0;
+        int since_poll = 0;  // nodes counted between the last two polls (dead-end monitor)
         int lim = 0;           // u loop: prune threshold minus |M|+1
         unsigned splits = 0;   // flushed to s.st_splits at polls and at the task's end
         bool abort_all = false;
@@ -338,8 +363,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 // deadend_check (heuristics.cpp:103-112) over the group's node count
                 int sus = 0;
                 if (lane == 0) {
-                    const unsigned long long total =
-                        atomicAdd(&gs->nodes, (unsigned long long)interval) + (unsigned long long)interval;
+                    const unsigned long long add = (unsigned long long)max(since_poll, 0);
+                    const unsigned long long total = atomicAdd(&gs->nodes, add) + add;
                     const unsigned long long at = *reinterpret_cast<volatile unsigned long long*>(&gs->at_improve);
                     const unsigned long long since = total - at;
                     sus = (p.deadend_abs && since >= p.deadend_abs) ||
@@ -359,7 +384,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             const int live = max(int(s.pf[20]), 1);
             const int total_warps = int(gridDim.x) * kWarpsPerCta;
             const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
+            // while many warps wait (a fresh launch with few roots), poll
+            // again soon: the launch fans out in tens of microseconds
+            if (waiting > total_warps / 4) cd = cd0 = kFastPoll;
             if ((waiting <= 0 && !starved) || d <= root) return true;
+            // The prefetched counters are one poll old: confirm with a fresh
+            // read before taking a producer ticket, so that the queue stays
+            // short (bounded by the warps racing here plus kStarvedQueue, far
+            // below the ring capacity: producers never wait on a full ring).
+            {
+                long long fresh = 0;
+                if (lane == 0) fresh = (long long)(ld_relaxed(&ctl->head.v) - ld_relaxed(&ctl->tail.v));
+                fresh = __shfl_sync(kFull, fresh, 0);
+                const bool starved_now = 2 * workers * live < total_warps && fresh > -kStarvedQueue;
+                if (fresh <= 0 && !starved_now) return true;
+            }
             // donate the shallowest level that still owns work
             int f = -1;
             for (int b0 = root; b0 < d && f < 0; b0 += 32) {
@@ -389,12 +428,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             // it; the ring is far larger than the warp count, so this wait is
             // normally zero.
             unsigned long long pos = 0;
+            int stalled = 0;
             if (lane == 0) {
                 atomicAdd(&ctl->pending.v, 1);
                 atomicAdd(&is->open_tasks, 1);
                 pos = atomicAdd(&ctl->tail.v, 1ull);
                 const Slot* sl = ring + (pos & p.cap_mask);
-                while (ld_acquire(&sl->seq) != pos) __nanosleep(32);
+                // watchdog: a slot that stays taken for 2 s means the ring
+                // invariant broke — stop the launch with an error, never hang
+                unsigned long long t_wait = 0, seq;
+                unsigned spins = 0;
+                while ((seq = ld_acquire(&sl->seq)) != pos) {
+                    __nanosleep(32);
+                    if ((++spins & 1023u) == 0) {
+                        const unsigned long long now = globaltimer();
+                        if (!t_wait) t_wait = now;
+                        else if (now - t_wait > p.ring_watchdog_ns) {
+                            Counters* c = p.counters;
+                            if (atomicAdd(&c->ring_stall, 1ull) == 0) {
+                                c->stall_pos = pos;
+                                c->stall_head = ld_relaxed(&ctl->head.v);
+                                c->stall_tail = ld_relaxed(&ctl->tail.v);
+                                c->stall_seq = seq;
+                            }
+                            atomicCAS(&ctl->stop.v, 0, 3);
+                            stalled = 1;
+                            break;
+                        }
+                    }
+                }
+            }
+            if (__shfl_sync(kFull, stalled, 0)) {
+                abort_all = true;
+                return false;
             }
             pos = __shfl_sync(kFull, pos, 0);
             Slot* sl = ring + (pos & p.cap_mask);
@@ -448,12 +514,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
 #define MCSG_COUNT_NODES(k)                                                     \
     cd -= (k);                                                                 \
     if (cd <= 0) {                                                             \
+        since_poll = cd0 - cd;                                                 \
         if (lane == 0) {                                                       \
-            s.polled += (unsigned long long)(long long)(interval - cd);        \
+            s.polled += (unsigned long long)(long long)since_poll;             \
             s.st_splits += splits;                                             \
         }                                                                      \
         splits = 0;                                                            \
-        cd = interval;                                                         \
+        cd = cd0 = interval;                                                   \
         if (!poll()) goto finish;                                              \
     }
 
@@ -597,7 +664,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             cd += int(__reduce_add_sync(kFull, unsigned(left))) + set_popc(cand) + (cont != 0);
         }
         if (lane == 0) {
-            const unsigned long long task_nodes = s.polled + (unsigned long long)(long long)(interval - cd);
+            const unsigned long long task_nodes = s.polled + (unsigned long long)(long long)(cd0 - cd);
             s.st_nodes += task_nodes;
             s.st_splits += splits;
             if (task_nodes) atomicAdd(&is->nodes, task_nodes);

@@ -1,0 +1,55 @@
+"""Launch robustness: the task ring's producer watchdog turns a stall into an
+error (never a hang), and the device stays usable afterwards.
+
+The stall is provoked with the library's test hooks: a 4-slot ring
+(MCSG_DEBUG_RING_CAP) makes producers wait for slots, and a zero watchdog
+(MCSG_DEBUG_RING_WATCHDOG_NS) makes any such wait fatal.
+"""
+import json
+import os
+
+import pytest
+
+import paper_1908_06418_b200 as M
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def c2_pairs(count):
+    out = []
+    for i in range(count):
+        k, j = i % 3, i // 3
+        s = 30000 + 1000 * k + 2 * j
+        p = (0.1, 0.3, 0.5)[k]
+        out.append((M.random_graph(30, p, s), M.random_graph(30, p, s + 1)))
+    return out
+
+
+def test_ring_stall_is_an_error_and_the_device_recovers(monkeypatch):
+    pairs = c2_pairs(6)
+    monkeypatch.setenv("MCSG_DEBUG_RING_CAP", "4")
+    monkeypatch.setenv("MCSG_DEBUG_RING_WATCHDOG_NS", "0")
+    stalled = False
+    for _ in range(5):
+        try:
+            M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+        except M.GraphError as e:
+            assert "task ring stalled" in str(e), e
+            stalled = True
+            break
+    assert stalled, "the debug ring never stalled"
+    monkeypatch.delenv("MCSG_DEBUG_RING_CAP")
+    monkeypatch.delenv("MCSG_DEBUG_RING_WATCHDOG_NS")
+    gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))["sizes"]
+    res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    assert [r.size for r in res] == [gold[str(i)] for i in range(6)]
+
+
+def test_small_ring_without_watchdog_is_still_exact(monkeypatch):
+    # a 64-slot ring: producers wait for consumers, results stay exact
+    pairs = c2_pairs(6)
+    monkeypatch.setenv("MCSG_DEBUG_RING_CAP", "64")
+    gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))["sizes"]
+    res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    assert [r.size for r in res] == [gold[str(i)] for i in range(6)]
