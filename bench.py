@@ -294,6 +294,18 @@ def run_ours(args, rank, world, local_rank):
         checked = [(i, s) for i, s in zip(idx, sizes_ref) if i in gold]
         golden_ok = all(gold[i] == s for i, s in checked) if checked else None
 
+    # Side measurement (N=1 only, outside the timed C2 region): time to the
+    # proven optimum of BASELINE.json configs[3]'s hard pair (C4, ER n=45
+    # p=0.5, seeds 45000/45001) on this GPU, every warp on one instance.
+    c4 = None
+    if rank == 0 and world == 1 and not args.no_c4:
+        g4, h4 = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
+        r4 = M.solve(g4, h4, M.SolveConfig(mode=M.MODE_THROUGHPUT, device=device, budget_seconds=120))
+        c4 = {"config": "C4: ER n=45 p=0.5 seeds 45000/45001 (BASELINE.json configs[3]), one GPU",
+              "status": r4.status.name, "size": r4.size, "time_to_optimum_s": r4.stats.kernel_seconds,
+              "nodes": r4.stats.recursions, "nodes_per_s": r4.stats.recursions / max(r4.stats.kernel_seconds, 1e-9),
+              "mapping_verified": bool(M.verify(g4, h4, r4.best))}
+
     t_dev = max_over_ranks(kernel_s)
     t_e2e = max_over_ranks(wall_s)
     total_nodes = sum_over_ranks(float(nodes))
@@ -349,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
                 "seconds_per_step": t_e2e / args.steps},
         "gpu_launches": launches,
         "roofline": roofline,
+        "c4_hard_instance": c4,
         "cpu_baseline": cpu_baseline,
         "clocks": clocks,
         "kernel": {"warps": st.warps, "ctas": st.ctas, "smem_per_cta": st.smem_per_cta,
@@ -371,6 +384,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=6.0, help="per-pair budget of the cpu_baseline sample")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="per-step budget of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 time-to-optimum side measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
