@@ -105,7 +105,7 @@ struct TaskHeader {
     uint8_t v;
     uint8_t bound;
     uint8_t cont;
-    uint8_t pad0;
+    uint8_t fanout;         // 1: donated while many warps waited (the receiver polls early)
     uint64_t cand;          // remaining u candidates (bitset over V_H)
     uint64_t pad1;
 };

@@ -459,6 +459,10 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.smem_classes = f.smem_classes;
     p.donate = parity ? 0 : 1;
     p.poll_interval = parity ? 4096 : 256;
+    if (const char* e = std::getenv("MCSG_DEBUG_POLL_INTERVAL")) {  // tests / experiments only
+        const int v = int(std::strtol(e, nullptr, 10));
+        if (v >= 1 && v <= 65536) p.poll_interval = v;
+    }
     p.counters = ctx.d_cnt;
     if (!parity && o.deadend_jump != 0) {  // the monitor only stops when a jump follows
         p.deadend_abs = o.deadend_abs;

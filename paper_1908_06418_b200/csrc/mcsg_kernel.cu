@@ -263,10 +263,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
 
         // nodes until the next poll (cd), counted from cd0; a throughput task
         // polls early once, and every kFastPoll nodes while warps wait for work
-        // a root task polls early: a launch with few roots starts fanning out
-        // at once (donated subtrees keep the normal interval: polling them
-        // early too floods the ring with tiny tasks)
-        int cd0 = (!PAR && !branch) ? kFastPoll : interval;
+        // a root task, and a subtree donated while many warps waited, polls
+        // early: a launch with few roots fans out in tens of microseconds
+        int cd0 = (!PAR && (!branch || hdr.fanout)) ? kFastPoll : interval;
         int cd = cd0;
         int since_poll = 0;  // nodes counted between the last two polls (dead-end monitor)
         int lim = 0;           // u loop: prune threshold minus |M|+1
@@ -339,6 +338,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             }
             const int gb = PAR ? 0 : int(s.pf[12]);  // GroupState::best
             const int gd = PAR ? 0 : int(s.pf[13]);  // GroupState::done
+            const int workers = int(s.pf[19]);      // InstanceState::workers
+            const int live = max(int(s.pf[20]), 1); // instances still open
+            // Every prefetched word is read above this barrier: the next
+            // prefetch rewrites the buffer asynchronously, and a word read
+            // after it could differ between lanes (a diverged warp).
             __syncwarp();
             prefetch_ctl();
             if (lane == 0 && st == 0) {
@@ -380,13 +384,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             // instances of a batch — when this instance runs on few warps and
             // the queue is short: a busy batch would otherwise never hand a
             // small instance's subtrees to anyone (FIFO tickets serve them next).
-            const int workers = int(s.pf[19]);
-            const int live = max(int(s.pf[20]), 1);
             const int total_warps = int(gridDim.x) * kWarpsPerCta;
             const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
             // while many warps wait (a fresh launch with few roots), poll
             // again soon: the launch fans out in tens of microseconds
-            if (waiting > total_warps / 4) cd = cd0 = kFastPoll;
+            const bool fanout = waiting > total_warps / 4;
+            if (fanout) cd = cd0 = kFastPoll;
             if ((waiting <= 0 && !starved) || d <= root) return true;
             // The prefetched counters are one poll old: confirm with a fresh
             // read before taking a producer ticket, so that the queue stays
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 h.v = uint8_t(fr_v(fw));
                 h.bound = uint8_t(fr_bound(fw));
                 h.cont = uint8_t(fr_cont(fw));
-                h.pad0 = 0;
+                h.fanout = fanout ? 1 : 0;
                 h.pad1 = 0;
                 X::put_cand(*sl, h, give);
                 sl->hdr = h;
