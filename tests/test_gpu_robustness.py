@@ -53,3 +53,17 @@ def test_small_ring_without_watchdog_is_still_exact(monkeypatch):
     gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))["sizes"]
     res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
     assert [r.size for r in res] == [gold[str(i)] for i in range(6)]
+
+
+def test_heavy_donation_stress_is_exact(monkeypatch):
+    # a 16-node poll interval: ~1M donations per 100-pair batch. This exposed a
+    # warp-divergence race (prefetched words read after the next prefetch was
+    # issued); the optima must stay exact and the launch must not fault.
+    pairs = c2_pairs(100)
+    monkeypatch.setenv("MCSG_DEBUG_POLL_INTERVAL", "16")
+    gold = json.load(open(os.path.join(HERE, "golden", "c2_sizes.json")))["sizes"]
+    for _ in range(2):
+        res, st = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+        assert [r.size for r in res] == [gold[str(i)] for i in range(100)]
+        assert all(r.status == M.SolveStatus.optimal for r in res)
+        assert st.donations > 100000
