@@ -97,6 +97,10 @@ inline SolveResult to_result(const mcsg_result& r, const mcsg_stats& st) {
     out.stats.recursions = r.nodes;
     out.stats.wall_seconds = st.wall_s;
     out.stats.probes = st.probes;
+    out.stats.tasks_published = st.donations;                    // subtrees handed to idle warps
+    out.stats.idle_seconds = double(st.idle_cycles) / 1.965e9;  // Σ warps' wait for work (B200 SM clock)
+    out.stats.deadend_suspects = (r.flags & MCSG_RESULT_SUSPECT) ? 1 : 0;
+    if (out.status == SolveStatus::optimal) out.stats.visited_ranges = 1;  // the whole tree, exactly once
     return out;
 }
 

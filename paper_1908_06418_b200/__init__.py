@@ -394,8 +394,24 @@ class SolveConfig:
 
 @dataclass
 class SearchStats:
+    """SearchStats (solve.hpp:27-55): the reference's fields first, mapped to
+    what the GPU engine measures; then the engine's own counters."""
     recursions: int = 0
     deadend_suspects: int = 0
+    # reference fields of the other engines (solve.hpp:35-52)
+    per_worker_recursions: list = field(default_factory=list)  # not kept per warp (thousands of warps)
+    idle_seconds: float = 0.0          # Σ over warps of the time spent waiting for a subtree
+    tasks_published: int = 0           # = donations (subtrees handed to idle warps)
+    iterations_total: int = 0          # parallel-engine iteration ledger: not applicable
+    iterations_executed: int = 0
+    iterations_pruned: int = 0
+    iteration_double_executions: int = 0
+    restore_checks: int = 0            # iterative-engine frame checks: not applicable
+    restore_violations: int = 0
+    peak_frames: int = 0
+    peak_frame_bytes: int = 0
+    restarts: int = 0                  # the GPU's restarts member diversifies order, it does not restart
+    visited_ranges: int = 0            # 1 for a completed search: the whole tree, exactly once
     wall_seconds: float = 0.0
     kernel_seconds: float = 0.0
     solve_seconds: float = 0.0
@@ -482,7 +498,14 @@ def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
         s.warps, s.ctas, s.smem_per_cta, s.smem_classes = st.warps, st.ctas, st.smem_per_cta, st.smem_classes
         s.h2d_bytes, s.d2h_bytes, s.launches = int(st.h2d_bytes), int(st.d2h_bytes), int(st.launches)
         s.busy_cycles, s.idle_cycles = int(st.busy_cycles), int(st.idle_cycles)
+        s.tasks_published = s.donations
+        s.idle_seconds = s.idle_cycles / _SM_HZ
+    if r.status == 0:
+        s.visited_ranges = 1
     return SolveResult(SolveStatus(r.status), pairs, int(r.size), s)
+
+
+_SM_HZ = 1.965e9  # B200 SM clock (MEASURED_PEAKS.json sm_max_mhz): idle cycles -> seconds
 
 
 def _check(rc: int):
