@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
             // while many warps wait (a fresh launch with few roots), poll
             // again soon: the launch fans out in tens of microseconds
-            const bool fanout = waiting > total_warps / 4;
+            const bool fanout = waiting > total_warps / 4;  // 2..32 measure alike (tools/fanout_sweep.sh)
             if (fanout) cd = cd0 = kFastPoll;
             if ((waiting <= 0 && !starved) || d <= root) return true;
             // The prefetched counters are one poll old: confirm with a fresh
