@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define MCSG_ABI_VERSION 2
+#define MCSG_ABI_VERSION 3
 
 /* status codes (mirror mcs_main.cpp:22-24 exit codes; SolveStatus solve.hpp:23) */
 #define MCSG_OPTIMAL 0
@@ -101,6 +101,12 @@ typedef struct mcsg_options {
     uint64_t deadend_abs;           /* 0 = off */
     double deadend_rel;             /* 0 = off */
     int32_t deadend_jump;           /* 0 none, 1 plus_one, 2 doubling */
+    /* Restarts (RestartConfig::multiplier, heuristics.hpp:90-102; throughput
+     * mode): when the nodes since the last improvement reach multiplier x
+     * max(1, nodes at that improvement), every warp freezes its open path
+     * into the task ring and resumes with the oldest queued subtree — the
+     * search stays complete. 0 = off. */
+    double restart_multiplier;
 } mcsg_options;
 
 #define MCSG_JUMP_PLUS_ONE 1
@@ -127,6 +133,8 @@ typedef struct mcsg_stats {
     uint64_t launches;       /* kernels launched by the call */
     uint64_t busy_cycles;    /* Σ over warps of SM cycles running tasks */
     uint64_t idle_cycles;    /* Σ over warps of SM cycles waiting for a task */
+    uint64_t restarts;       /* restart events (group 0 of the call) */
+    uint64_t frozen;         /* subtrees frozen into the ring by restarts */
 } mcsg_stats;
 
 typedef struct mcsg_result {

@@ -97,7 +97,8 @@ class _Options(C.Structure):
                 ("device", C.c_int32), ("max_warps", C.c_int32), ("smem_classes", C.c_int32),
                 ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32)),
                 ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32),
-                ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32)]
+                ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32),
+                ("restart_multiplier", C.c_double)]
 
 
 class _Stats(C.Structure):
@@ -107,7 +108,8 @@ class _Stats(C.Structure):
                 ("kernel_s", C.c_double), ("h2d_s", C.c_double), ("warps", C.c_int32),
                 ("ctas", C.c_int32), ("smem_per_cta", C.c_int32), ("smem_classes", C.c_int32),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64),
-                ("busy_cycles", C.c_uint64), ("idle_cycles", C.c_uint64)]
+                ("busy_cycles", C.c_uint64), ("idle_cycles", C.c_uint64),
+                ("restarts", C.c_uint64), ("frozen", C.c_uint64)]
 
 
 class _Result(C.Structure):
@@ -390,6 +392,7 @@ class SolveConfig:
     frontier: int = 0                  # host-expanded subtrees per device (0 = 256)
     deadend: tuple | None = None       # ("abs", n) | ("rel", mult): DeadEndPolicy
     deadend_jump: "JumpMode | None" = None  # jump that resumes after a suspect verdict
+    restart_multiplier: float = 0.0    # RestartConfig::multiplier (throughput mode); 0 = no restarts
 
 
 @dataclass
@@ -410,7 +413,8 @@ class SearchStats:
     restore_violations: int = 0
     peak_frames: int = 0
     peak_frame_bytes: int = 0
-    restarts: int = 0                  # the GPU's restarts member diversifies order, it does not restart
+    restarts: int = 0                  # restart events (restart_multiplier > 0; restarts.cpp:35-246)
+    frozen: int = 0                    # open-path subtrees frozen into the ring by those restarts
     visited_ranges: int = 0            # 1 for a completed search: the whole tree, exactly once
     wall_seconds: float = 0.0
     kernel_seconds: float = 0.0
@@ -479,6 +483,7 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
             raise GraphError(f"unknown deadend policy '{kind}'")
         if cfg.deadend_jump is not None:
             o.deadend_jump = 2 if cfg.deadend_jump == JumpMode.doubling else 1
+    o.restart_multiplier = float(cfg.restart_multiplier)
     for k, v in over.items():
         setattr(o, k, v)
     return o
@@ -499,6 +504,7 @@ def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
         s.h2d_bytes, s.d2h_bytes, s.launches = int(st.h2d_bytes), int(st.d2h_bytes), int(st.launches)
         s.busy_cycles, s.idle_cycles = int(st.busy_cycles), int(st.idle_cycles)
         s.tasks_published = s.donations
+        s.restarts, s.frozen = int(st.restarts), int(st.frozen)
         s.idle_seconds = s.idle_cycles / _SM_HZ
     if r.status == 0:
         s.visited_ranges = 1
@@ -663,7 +669,10 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
     recursive / iterative -> parity mode (reference node order);
     parallel / gpu       -> throughput mode (all warps, donation);
     goal / jump          -> GPU goal probes; restarts:<seed> -> throughput mode
-    with that seed. Orderings are applied host-side around every engine.
+    with that seed's search order and the reference's restart rule
+    (RestartConfig::multiplier = 2: every warp freezes its open path into
+    the ring when the nodes since the last improvement reach twice the nodes
+    at it). Orderings are applied host-side around every engine.
     """
     import dataclasses
     cfg = dataclasses.replace(config or SolveConfig(), order=spec.order)
@@ -679,7 +688,8 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
     if spec.goal_directed:
         return solve_goal_directed(g, h, cfg)
     if spec.restart_seed is not None:
-        return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, seed=spec.restart_seed))
+        return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, seed=spec.restart_seed,
+                                               restart_multiplier=2.0))
     if spec.deadend is not None:
         # forecast-then-mitigate (portfolio.cpp:136-155): a monitored all-warp
         # solve; with a jump configured, a suspect verdict hands the incumbent

@@ -86,7 +86,7 @@ struct alignas(16) GroupState {
     int32_t reached;        // goal probes: 1 when |M| >= goal was found
     // dead-end monitor (heuristics.hpp:30-60), only when a policy is set
     uint32_t suspect;       // 1: the policy fired and stopped the search
-    uint32_t pad;
+    uint32_t epoch;         // restarts so far (RestartDriver, restarts.cpp:35-246)
     unsigned long long nodes;       // nodes counted so far (per poll interval)
     unsigned long long at_improve;  // `nodes` when the incumbent last improved
 };
@@ -145,6 +145,7 @@ struct Counters {
     unsigned long long overflow;     // class-stack overflow (must stay 0)
     unsigned long long ring_stall;   // a producer waited > 2 s for a ring slot (must stay 0)
     unsigned long long bad_task;     // a consumed subtree had an impossible header (must stay 0)
+    unsigned long long frozen;       // subtrees frozen into the ring by restarts
     unsigned long long stall_pos, stall_head, stall_tail, stall_seq;  // its ticket and the ring state
     unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
     unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks
@@ -201,6 +202,12 @@ struct KernelParams {
     // reach deadend_abs, or deadend_rel * max(1, nodes at the improvement)
     unsigned long long deadend_abs;  // 0 = off
     double deadend_rel;              // 0 = off
+    // Restarts (RestartConfig::multiplier, heuristics.hpp:90-102): a restart
+    // is due when the group's nodes since its last improvement reach
+    // restart_mult x max(1, nodes at that improvement); every warp of the
+    // group then freezes its open path into the ring (exactly-once segments)
+    // and resumes with the oldest queued subtree. 0 = off.
+    double restart_mult;
 };
 
 }  // namespace mcsg

@@ -203,6 +203,7 @@ struct GroupResult {
     int winner = -1;
     bool reached = false;
     bool suspect = false;
+    uint32_t restarts = 0;
 };
 
 struct LaunchOut {
@@ -464,6 +465,7 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
         if (v >= 1 && v <= 65536) p.poll_interval = v;
     }
     p.counters = ctx.d_cnt;
+    if (!parity) p.restart_mult = o.restart_multiplier;
     if (!parity && o.deadend_jump != 0) {  // the monitor only stops when a jump follows
         p.deadend_abs = o.deadend_abs;
         p.deadend_rel = o.deadend_rel;
@@ -528,6 +530,7 @@ LaunchOut finish(InFlight& f) {
         out.groups[gi].winner = ctx.h_grp[gi].winner;
         out.groups[gi].reached = ctx.h_grp[gi].reached != 0;
         out.groups[gi].suspect = ctx.h_grp[gi].suspect != 0;
+        out.groups[gi].restarts = ctx.h_grp[gi].epoch;
     }
     for (int i = 0; i < n; ++i) {
         const InstanceState& s = ctx.h_ist[i];
@@ -743,6 +746,8 @@ void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probe
     st->launches = lo.launches;
     st->busy_cycles = lo.counters.busy_cycles;
     st->idle_cycles = lo.counters.idle_cycles;
+    st->restarts = lo.groups.empty() ? 0 : lo.groups[0].restarts;
+    st->frozen = lo.counters.frozen;
 }
 
 void accumulate(mcsg_stats* st, const LaunchOut& lo) {
@@ -765,6 +770,8 @@ void accumulate(mcsg_stats* st, const LaunchOut& lo) {
     st->launches += lo.launches;
     st->busy_cycles += lo.counters.busy_cycles;
     st->idle_cycles += lo.counters.idle_cycles;
+    st->restarts += lo.groups.empty() ? 0 : lo.groups[0].restarts;
+    st->frozen += lo.counters.frozen;
 }
 
 mcsg_options defaults(const mcsg_options* o) {

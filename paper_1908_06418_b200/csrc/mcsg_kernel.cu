@@ -37,7 +37,9 @@ constexpr int kStarvedQueue = 256;
 // Poll interval (nodes) while warps are waiting for work.
 constexpr int kFastPoll = 16;
 
-template <class X, bool PAR>
+// RST: restarts compiled in (throughput mode with restart_mult > 0 only), so
+// that the common launch carries none of their code.
+template <class X, bool PAR, bool RST = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
     mcs_search_kernel(KernelParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
     int maxp = 0, goal = 0, prune = 1, floor_sz = 0, grp = 0;
     bool stop_all = false;
     bool have_ticket = false;
+    int my_epoch = 0;  // restart epoch of the group when this warp last looked (RST only)
     unsigned long long ticket = 0;
 
     while (!stop_all) {
@@ -190,13 +193,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
         int best_local = 0, best_eff = floor_sz;
         bool skip = false;
         {
-            int gb = 0, gd = 0;
+            int gb = 0, gd = 0, ge = 0;
             if (lane == 0) {
                 gb = int(ld_volatile_u(&gs->best));
                 gd = int(ld_volatile_u(&gs->done));
+                ge = int(ld_volatile_u(&gs->epoch));
             }
             gb = __shfl_sync(kFull, gb, 0);
             gd = __shfl_sync(kFull, gd, 0);
+            my_epoch = __shfl_sync(kFull, ge, 0);
             if (!PAR) best_eff = max(best_eff, gb);
             skip = gd != 0;
         }
@@ -309,7 +314,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                     __threadfence();
                     atomicMax(&gs->best, unsigned(dd + 1));
                     // DeadEndMonitor::note_improvement (heuristics.hpp:45)
-                    if (p.deadend_abs || p.deadend_rel > 0.0)
+                    // (restarts.cpp:91: at_improvement = nodes on improvement)
+                    if (p.deadend_abs || p.deadend_rel > 0.0 || (RST && p.restart_mult > 0.0))
                         atomicMax(&gs->at_improve, *reinterpret_cast<volatile unsigned long long*>(&gs->nodes));
                 }
                 // push the size to the other devices' incumbents (NVLink P2P)
@@ -322,106 +328,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             }
         };
 
-        // Periodic poll: stop/deadline/cancel, group done, shared incumbent,
-        // and subtree donation to idle warps. Returns false to end the task.
-        auto poll = [&]() -> bool {
-            // values prefetched at the previous poll (one interval stale: stale
-            // reads only delay a stop or weaken pruning, SPEC.md:280)
-            cp_async_wait_all();
-            __syncwarp();
-            int st = int(s.pf[0]);
-            long long waiting = 0;  // warps holding a ticket no producer has served yet
-            if (!PAR) {
-                const unsigned long long hd = (unsigned long long)s.pf[4] | ((unsigned long long)s.pf[5] << 32);
-                const unsigned long long tl = (unsigned long long)s.pf[8] | ((unsigned long long)s.pf[9] << 32);
-                waiting = (long long)(hd - tl);
-            }
-            const int gb = PAR ? 0 : int(s.pf[12]);  // GroupState::best
-            const int gd = PAR ? 0 : int(s.pf[13]);  // GroupState::done
-            const int workers = int(s.pf[19]);      // InstanceState::workers
-            const int live = max(int(s.pf[20]), 1); // instances still open
-            // Every prefetched word is read above this barrier: the next
-            // prefetch rewrites the buffer asynchronously, and a word read
-            // after it could differ between lanes (a diverged warp).
-            __syncwarp();
-            prefetch_ctl();
-            if (lane == 0 && st == 0) {
-                if (deadline && globaltimer() >= deadline) {
-                    atomicCAS(&ctl->stop.v, 0, 1);
-                    st = 1;
-                }
-                if (st == 0 && gw == 0 && p.cancel && *p.cancel) {
-                    atomicCAS(&ctl->stop.v, 0, 2);
-                    st = 2;
-                }
-            }
-            st = __shfl_sync(kFull, st, 0);
-            if (st != 0) {
-                abort_all = true;
-                return false;
-            }
-            if (PAR) return true;
-            if (gd != 0) return false;
-            if (gb > best_eff) raise_best(gb);
-            if (p.deadend_abs || p.deadend_rel > 0.0) {
-                // deadend_check (heuristics.cpp:103-112) over the group's node count
-                int sus = 0;
-                if (lane == 0) {
-                    const unsigned long long add = (unsigned long long)max(since_poll, 0);
-                    const unsigned long long total = atomicAdd(&gs->nodes, add) + add;
-                    const unsigned long long at = *reinterpret_cast<volatile unsigned long long*>(&gs->at_improve);
-                    const unsigned long long since = total - at;
-                    sus = (p.deadend_abs && since >= p.deadend_abs) ||
-                          (p.deadend_rel > 0.0 && double(since) >= p.deadend_rel * double(at > 0 ? at : 1ull));
-                    if (sus) {
-                        gs->suspect = 1u;
-                        atomicExch(&gs->done, 1u);
-                    }
-                }
-                if (__shfl_sync(kFull, sus, 0)) return false;
-            }
-            // Donate when warps wait for work, or — fairness between the
-            // instances of a batch — when this instance runs on few warps and
-            // the queue is short: a busy batch would otherwise never hand a
-            // small instance's subtrees to anyone (FIFO tickets serve them next).
-            const int total_warps = int(gridDim.x) * kWarpsPerCta;
-            const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
-            // while many warps wait (a fresh launch with few roots), poll
-            // again soon: the launch fans out in tens of microseconds
-            const bool fanout = waiting > total_warps / 4;  // 2..32 measure alike (tools/fanout_sweep.sh)
-            if (fanout) cd = cd0 = kFastPoll;
-            if ((waiting <= 0 && !starved) || d <= root) return true;
-            // The prefetched counters are one poll old: confirm with a fresh
-            // read before taking a producer ticket, so that the queue stays
-            // short (bounded by the warps racing here plus kStarvedQueue, far
-            // below the ring capacity: producers never wait on a full ring).
-            {
-                long long fresh = 0;
-                if (lane == 0) fresh = (long long)(ld_relaxed(&ctl->head.v) - ld_relaxed(&ctl->tail.v));
-                fresh = __shfl_sync(kFull, fresh, 0);
-                const bool starved_now = 2 * workers * live < total_warps && fresh > -kStarvedQueue;
-                if (fresh <= 0 && !starved_now) return true;
-            }
-            // donate the shallowest level that still owns work
-            int f = -1;
-            for (int b0 = root; b0 < d && f < 0; b0 += 32) {
-                const int lv = b0 + lane;
-                bool has = false;
-                if (lv < d) has = set_any(s.f_cand[lv]) || fr_cont(s.f_word[lv]);
-                const unsigned m = __ballot_sync(kFull, has);
-                if (m) f = b0 + __ffs(m) - 1;
-            }
-            if (f < 0) return true;
+        // Hands level f's remaining u candidates (all of them, or the half
+        // the donor would reach last) and its continuation to the ring as a
+        // frozen subtree. False when the producer watchdog fired (abort).
+        auto donate_level = [&](int f, bool all, bool fanout) -> bool {
             const W fc = s.f_cand[f];
             const unsigned long long fw = s.f_word[f];
             const int cnt = set_popc(fc);
             // hand over the half the donor would reach last (throughput mode
             // walks u from the top: the lower half)
             W keep = fc;
-            if (cnt >= 2)
-                for (int i = 0; i < cnt / 2; ++i) keep = set_drop_lowest(keep);
-            else
+            if (all || cnt < 2)
                 keep = W{};
+            else
+                for (int i = 0; i < cnt / 2; ++i) keep = set_drop_lowest(keep);
             const W give = set_andnot(fc, keep);
             // the donor counted these children (and the continuation) when it
             // selected level f; the receiver counts them when it resumes
@@ -508,6 +428,137 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             return true;
         };
 
+        // Periodic poll: stop/deadline/cancel, group done, shared incumbent,
+        // and subtree donation to idle warps. Returns false to end the task.
+        auto poll = [&]() -> bool {
+            // values prefetched at the previous poll (one interval stale: stale
+            // reads only delay a stop or weaken pruning, SPEC.md:280)
+            cp_async_wait_all();
+            __syncwarp();
+            int st = int(s.pf[0]);
+            long long waiting = 0;  // warps holding a ticket no producer has served yet
+            if (!PAR) {
+                const unsigned long long hd = (unsigned long long)s.pf[4] | ((unsigned long long)s.pf[5] << 32);
+                const unsigned long long tl = (unsigned long long)s.pf[8] | ((unsigned long long)s.pf[9] << 32);
+                waiting = (long long)(hd - tl);
+            }
+            const int gb = PAR ? 0 : int(s.pf[12]);  // GroupState::best
+            const int gd = PAR ? 0 : int(s.pf[13]);  // GroupState::done
+            const int workers = int(s.pf[19]);      // InstanceState::workers
+            const int live = max(int(s.pf[20]), 1); // instances still open
+            // Every prefetched word is read above this barrier: the next
+            // prefetch rewrites the buffer asynchronously, and a word read
+            // after it could differ between lanes (a diverged warp).
+            __syncwarp();
+            prefetch_ctl();
+            if (lane == 0 && st == 0) {
+                if (deadline && globaltimer() >= deadline) {
+                    atomicCAS(&ctl->stop.v, 0, 1);
+                    st = 1;
+                }
+                if (st == 0 && gw == 0 && p.cancel && *p.cancel) {
+                    atomicCAS(&ctl->stop.v, 0, 2);
+                    st = 2;
+                }
+            }
+            st = __shfl_sync(kFull, st, 0);
+            if (st != 0) {
+                abort_all = true;
+                return false;
+            }
+            if (PAR) return true;
+            if (gd != 0) return false;
+            if (gb > best_eff) raise_best(gb);
+            if (p.deadend_abs || p.deadend_rel > 0.0 || (RST && p.restart_mult > 0.0)) {
+                // the group's node count since its last improvement drives
+                // deadend_check (heuristics.cpp:103-112) and restart_due
+                // (restarts.cpp:66-70)
+                int sus = 0, ep = my_epoch;
+                if (lane == 0) {
+                    const unsigned long long add = (unsigned long long)max(since_poll, 0);
+                    const unsigned long long total = atomicAdd(&gs->nodes, add) + add;
+                    const unsigned long long at = *reinterpret_cast<volatile unsigned long long*>(&gs->at_improve);
+                    const unsigned long long since = total - at;
+                    sus = (p.deadend_abs && since >= p.deadend_abs) ||
+                          (p.deadend_rel > 0.0 && double(since) >= p.deadend_rel * double(at > 0 ? at : 1ull));
+                    if (sus) {
+                        gs->suspect = 1u;
+                        atomicExch(&gs->done, 1u);
+                    }
+                    // a restart is due: the first warp to see it rearms the
+                    // monitor (at_improvement = nodes) and opens a new epoch
+                    if (RST && p.restart_mult > 0.0 && double(since) >= p.restart_mult * double(at > 0 ? at : 1ull) &&
+                        atomicCAS(&gs->at_improve, at, total) == at)
+                        atomicAdd(&gs->epoch, 1u);
+                    ep = int(ld_volatile_u(&gs->epoch));
+                }
+                if (__shfl_sync(kFull, sus, 0)) return false;
+                ep = __shfl_sync(kFull, ep, 0);
+                if (RST && ep != my_epoch) {
+                    my_epoch = ep;
+                    // Restart: freeze the open path — every level with work,
+                    // the current one included — into the ring as frozen
+                    // subtrees (the pool of segments, restarts.cpp:80-97),
+                    // end this task, and take the oldest queued subtree next.
+                    // Skipped when the ring lacks room (the search stays
+                    // complete either way).
+                    long long queued = 0;
+                    if (lane == 0) queued = (long long)(ld_relaxed(&ctl->tail.v) - ld_relaxed(&ctl->head.v));
+                    queued = __shfl_sync(kFull, queued, 0);
+                    // (only once the current node is selected: the root
+                    // count's poll comes before its select)
+                    if ((set_any(cand) || cont) && queued + (d - root + 1) < (long long)(p.cap_mask + 1) / 2) {
+                        s.f_cand[d] = cand;  // the current level becomes a frame like the others
+                        s.f_word[d] = pack_frame(base, nc, sel, v, bound, cont, 0);
+                        __syncwarp();
+                        int frozen = 0;
+                        for (int lv = root; lv <= d; ++lv) {
+                            if (!set_any(s.f_cand[lv]) && !fr_cont(s.f_word[lv])) continue;
+                            if (!donate_level(lv, true, false)) return false;
+                            ++frozen;
+                        }
+                        cand = W{};
+                        cont = 0;
+                        if (lane == 0) atomicAdd(&p.counters->frozen, (unsigned long long)frozen);
+                        return false;
+                    }
+                }
+            }
+            // Donate when warps wait for work, or — fairness between the
+            // instances of a batch — when this instance runs on few warps and
+            // the queue is short: a busy batch would otherwise never hand a
+            // small instance's subtrees to anyone (FIFO tickets serve them next).
+            const int total_warps = int(gridDim.x) * kWarpsPerCta;
+            const bool starved = 2 * workers * live < total_warps && waiting > -kStarvedQueue;
+            // while many warps wait (a fresh launch with few roots), poll
+            // again soon: the launch fans out in tens of microseconds
+            const bool fanout = waiting > total_warps / 4;  // 2..32 measure alike (tools/fanout_sweep.sh)
+            if (fanout) cd = cd0 = kFastPoll;
+            if ((waiting <= 0 && !starved) || d <= root) return true;
+            // The prefetched counters are one poll old: confirm with a fresh
+            // read before taking a producer ticket, so that the queue stays
+            // short (bounded by the warps racing here plus kStarvedQueue, far
+            // below the ring capacity: producers never wait on a full ring).
+            {
+                long long fresh = 0;
+                if (lane == 0) fresh = (long long)(ld_relaxed(&ctl->head.v) - ld_relaxed(&ctl->tail.v));
+                fresh = __shfl_sync(kFull, fresh, 0);
+                const bool starved_now = 2 * workers * live < total_warps && fresh > -kStarvedQueue;
+                if (fresh <= 0 && !starved_now) return true;
+            }
+            // donate the shallowest level that still owns work
+            int f = -1;
+            for (int b0 = root; b0 < d && f < 0; b0 += 32) {
+                const int lv = b0 + lane;
+                bool has = false;
+                if (lv < d) has = set_any(s.f_cand[lv]) || fr_cont(s.f_word[lv]);
+                const unsigned m = __ballot_sync(kFull, has);
+                if (m) f = b0 + __ffs(m) - 1;
+            }
+            if (f < 0) return true;
+            return donate_level(f, false, fanout);
+        };
+
 // Node counting (search_core.hpp:130). Nodes are counted in bulk when a level
 // is selected: its |R*| children and its continuation are all counted nodes
 // (each is entered, even when its bound prunes it at once), so the u loop
@@ -534,7 +585,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 if (bound <= prn_thr) goto pop;
                 goto select;
             }
-            // a donated subtree: its remaining children and continuation
+            // a donated subtree: its remaining children and continuation (the
+            // level's first-child offer happened in the donor)
             cd -= set_popc(cand) + (cont != 0);
             goto next;
 
@@ -551,11 +603,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 cont = kContOwned | (set_popc(lsel) <= set_popc(cand) ? kContDec : 0);
             }
             x.prep_v(v, sel);
-            MCSG_COUNT_NODES(set_popc(cand) + 1);  // the children and the continuation
             // Incumbent offer at the entry of the level's first child
             // (search_core.hpp:145-155). Only a first child can improve: once
             // it is entered the threshold is >= d+1 for its siblings, for
-            // later selects at this depth and after every pop back here.
+            // later selects at this depth and after every pop back here. It
+            // runs before the level's nodes are counted (so a restart that
+            // freezes the level at the count's poll finds the offer done); a
+            // stop here counts the one child it entered.
             if (d + 1 > off_thr) {
                 const int u = PAR ? set_ctz(cand) : set_top(cand);
                 offer(d, u);
@@ -571,10 +625,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                         if (goal_hit) atomicExch_system(&p.peer_grp[lane]->reached, 1);
                         atomicExch_system(&p.peer_grp[lane]->done, 1u);
                     }
-                    cand = set_without(cand, u);  // u was entered; the rest never is
+                    cd -= 1;  // u was entered; nothing else of this level is
+                    cand = W{};
+                    cont = 0;
                     goto finish;
                 }
             }
+            MCSG_COUNT_NODES(set_popc(cand) + 1);  // the children and the continuation
 
         next:
             // ---- u loop (search_core.hpp:183-200): children in ascending u
@@ -706,12 +763,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
 // ------------------------------------------------------------ host launch --
 // Kernel flavours by bitset width: 32 (n <= 32), 64 (n <= 64), and the wide
 // policies 128 (n <= 128) and 256 (n <= 255).
-template <class X, bool PAR>
+template <class X, bool PAR, bool RST = false>
 static cudaError_t launch_t(const KernelParams& p, int ctas, cudaStream_t st) {
     const int smem = warp_smem_bytes<X>(p.smem_classes) * kWarpsPerCta;
-    cudaError_t e = cudaFuncSetAttribute(mcs_search_kernel<X, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(mcs_search_kernel<X, PAR, RST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    mcs_search_kernel<X, PAR><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
+    mcs_search_kernel<X, PAR, RST><<<ctas, kWarpsPerCta * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -719,8 +777,9 @@ template <class X>
 static int occupancy_t(int smem_classes) {
     const int smem = warp_smem_bytes<X>(smem_classes) * kWarpsPerCta;
     int worst = 1 << 30;
-    for (int par = 0; par < 2; ++par) {
-        auto fn = par ? mcs_search_kernel<X, true> : mcs_search_kernel<X, false>;
+    for (int par = 0; par < 3; ++par) {
+        auto fn = par == 1 ? mcs_search_kernel<X, true> : par == 2 ? mcs_search_kernel<X, false, true>
+                                                                   : mcs_search_kernel<X, false>;
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
         int blocks = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kWarpsPerCta * 32, smem) != cudaSuccess)
@@ -767,7 +826,8 @@ int kernel_occupancy(int bits, bool directed, int smem_classes) {
 
 cudaError_t kernel_launch(int bits, bool directed, bool parity, const KernelParams& p, int ctas, cudaStream_t st) {
     return with_policy(bits, directed, [&]<class X>() {
-        return parity ? launch_t<X, true>(p, ctas, st) : launch_t<X, false>(p, ctas, st);
+        if (parity) return launch_t<X, true>(p, ctas, st);
+        return p.restart_mult > 0.0 ? launch_t<X, false, true>(p, ctas, st) : launch_t<X, false>(p, ctas, st);
     });
 }
 
