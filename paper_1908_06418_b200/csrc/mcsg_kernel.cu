@@ -4,27 +4,30 @@
 // donated subtree from the HBM ring), run its DFS, finish it. The DFS itself:
 //
 //   select  choose the label class (min max(|L|,|R|), label_classes.cpp:47-67)
-//           and the vertex v (max degree, label_classes.cpp:69-78)
-//   next    for each u of the class's right side in ascending id
-//           (search_core.hpp:183-200): count the child node, offer its
-//           mapping when it improves (search_core.hpp:145-155), compute its
-//           bound from the register-resident level (label_classes.cpp:41-45)
-//           and only when it survives the prune test (search_core.hpp:166)
-//           materialise it with filter_classes (label_classes.cpp:80-108)
-//           and descend
-//   cont    then the "v unmatched" continuation at the same level, itself a
-//           counted node (search_core.hpp:201-212)
+//           and the vertex v (max degree, label_classes.cpp:69-78); offer
+//           the first child's mapping when it improves
+//           (search_core.hpp:145-155); count the level's |R*| children and
+//           its continuation in bulk (each is a counted node,
+//           search_core.hpp:130) and poll
+//   next    for each u of the class's right side (search_core.hpp:183-200):
+//           compute the child's bound from the register-resident level
+//           (label_classes.cpp:41-45) and only when it survives the prune
+//           test (search_core.hpp:166) materialise it with filter_classes
+//           (label_classes.cpp:80-108) and descend
+//   cont    then the "v unmatched" continuation at the same level
+//           (search_core.hpp:201-212)
 //   pop     back to the parent level
 //
-// Two specialisations:
-//   PAR = true   parity mode: one warp per instance, no donation; the host
-//                keeps the reference's vertex ids so the DFS visits the
-//                reference's nodes in the reference's order (tests compare
-//                node counts and mappings exactly).
+// Specialisations:
+//   PAR = true   parity mode: one warp per instance, no donation, u in
+//                ascending id; the host keeps the reference's vertex ids so
+//                the DFS visits the reference's nodes in the reference's
+//                order (tests compare node counts and mappings exactly).
 //   PAR = false  throughput mode: every resident warp, subtree donation to
-//                idle warps, group incumbent shared through HBM. The host
-//                relabels G in (degree desc, id asc) order so select_vertex
-//                is a single ctz; class ties break on that order.
+//                idle warps, group incumbent shared through HBM, u walked
+//                from the top. The host relabels G in REVERSE (degree desc,
+//                id asc) order so select_vertex is a single FLO.
+//   RST = true   throughput mode with restarts (restart_mult > 0).
 #include "mcsg_search.cuh"
 
 namespace mcsg {
