@@ -1,4 +1,5 @@
 """Measures how many 64-bit-kernel nodes sit at levels whose live vertex sets fit 32 bits (needs a build with the EXPERIMENT block described in DESIGN §9; dev tool)."""
+import sys, json
 sys.path.insert(0, '.')
 import paper_1908_06418_b200 as M
 g, h = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
