@@ -325,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
     inst_per_node = prof.get("warp_inst_per_node")
     import hashlib
     sha = hashlib.sha1()
-    for f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_device.h"):
+    for f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_task_body.inc", "mcsg_device.h"):
         with open(os.path.join(ROOT, "paper_1908_06418_b200", "csrc", f), "rb") as fh:
             sha.update(fh.read())
     profile_current = prof.get("kernel_src_sha1") == sha.hexdigest()

@@ -146,6 +146,7 @@ struct Counters {
     unsigned long long ring_stall;   // a producer waited > 2 s for a ring slot (must stay 0)
     unsigned long long bad_task;     // a consumed subtree had an impossible header (must stay 0)
     unsigned long long frozen;       // subtrees frozen into the ring by restarts
+    unsigned long long nests_smem, nests_hbm;  // compacted subtrees (64-bit kernel)
     unsigned long long stall_pos, stall_head, stall_tail, stall_seq;  // its ticket and the ring state
     unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
     unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks
@@ -208,6 +209,13 @@ struct KernelParams {
     // group then freezes its open path into the ring (exactly-once segments)
     // and resumes with the oldest queued subtree. 0 = off.
     double restart_mult;
+    // 64-bit kernel: run subtrees whose live vertex sets fit 32 bits with
+    // the 32-bit policy (CompactSearch, nested in the task): a level is
+    // compacted when its bound exceeds the prune threshold by at least
+    // `compact` (a small slack means a small subtree, where the compaction
+    // costs more than it saves); 0 = off
+    int32_t compact;
+    int32_t compact_hbm;  // the compact stack may sit in the HBM spill area (2: always, a test knob)
 };
 
 }  // namespace mcsg

@@ -446,6 +446,13 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     }
     p.cap_mask = cap - 1;
     p.ring_watchdog_ns = 2000000000ull;
+    // compacted subtrees (64-bit kernel): slack 3 (C4 5.3 s at 2, 5.4 at 4;
+    // C3 0.55 s at 2, 0.53 at 4; every nest costs ≈ 600 warp-instructions)
+    p.compact = 3;
+    p.compact_hbm = 1;
+    if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_HBM")) p.compact_hbm = int(std::strtol(e, nullptr, 10));
+    if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_SLACK")) p.compact = std::max(1, int(std::strtol(e, nullptr, 10)));
+    if (const char* e = std::getenv("MCSG_DEBUG_NO_COMPACT")) p.compact = (e[0] == '0') ? p.compact : 0;
     if (const char* e = std::getenv("MCSG_DEBUG_RING_WATCHDOG_NS")) p.ring_watchdog_ns = std::strtoull(e, nullptr, 10);
     p.n_inst = n;
     p.n_roots = ex.roots ? n : 0;
@@ -748,6 +755,8 @@ void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probe
     st->idle_cycles = lo.counters.idle_cycles;
     st->restarts = lo.groups.empty() ? 0 : lo.groups[0].restarts;
     st->frozen = lo.counters.frozen;
+    if (std::getenv("MCSG_DEBUG_NESTS"))
+        std::fprintf(stderr, "nests smem %llu hbm %llu\n", lo.counters.nests_smem, lo.counters.nests_hbm);
 }
 
 void accumulate(mcsg_stats* st, const LaunchOut& lo) {

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "mcsg_device.h"
 
@@ -234,6 +235,29 @@ __device__ __forceinline__ int fr_bound(unsigned long long f) { return int(__byt
 __device__ __forceinline__ int fr_cont(unsigned long long f) { return int(__byte_perm(unsigned(f >> 32), 0, 0x4442)); }
 __device__ __forceinline__ int fr_u(unsigned long long f) { return int(unsigned(f >> 32) >> 24); }
 
+template <typename W, bool DIR>
+struct WarpSmem;
+
+// The 64-bit kernel's area for a subtree compacted to 32 bits: a 32-bit
+// search image (rows of the live vertices, renumbered 0..31) and the maps
+// between compact and original ids.
+struct NoCompactArea {};
+template <bool DIR>
+struct CompactRows {  // what the 32-bit policy reads through its `s`
+    uint32_t out_g[32];
+    uint32_t out_h[32];
+    uint32_t in_g[DIR ? 32 : 1];
+    uint32_t in_h[DIR ? 32 : 1];
+    uint16_t vkey[32];  // (parity mode only; compaction runs in throughput mode)
+};
+template <bool DIR>
+struct CompactArea {
+    CompactRows<DIR> img;            // rows of the live vertices, renumbered
+    uint8_t gid[32], hid[32];        // compact id -> original id
+    uint8_t cmap_g[64], cmap_h[64];  // original id -> compact id
+    unsigned long long nests_smem, nests_hbm;  // subtrees run compacted, by stack placement
+};
+
 // Per-warp shared-memory image; the class stack follows it.
 template <typename W, bool DIR>
 struct WarpSmem {
@@ -256,6 +280,8 @@ struct WarpSmem {
     uint16_t vkey[NB];
     uint8_t map_v[kMaxDepth + 1];  // mapping prefix below the task's root level
     uint8_t map_u[kMaxDepth + 1];
+    // 64-bit kernel only: a subtree compacted to 32 bits (CompactSearch)
+    [[no_unique_address]] std::conditional_t<sizeof(W) == 8, CompactArea<DIR>, NoCompactArea> ca;
 };
 
 // Per-warp shared memory of a search policy X: its fixed image, then the
@@ -274,7 +300,7 @@ __host__ __device__ constexpr int warp_smem_bytes(int classes) {
 //
 // The kernel body (mcsg_kernel.cu) is written against this policy interface;
 // WideSearch below implements the same interface for 64 < n <= 255.
-template <typename W, bool DIR>
+template <typename W, bool DIR, class SmT = WarpSmem<W, DIR>>
 struct Search {
     static constexpr int S = Bits<W>::slots;
     static constexpr int NB = Bits<W>::n;
@@ -283,8 +309,12 @@ struct Search {
 #define MCSG_U64_MIN_BLOCKS 7  // 72 registers, 28 warps/SM: +2.6% on C4 over 6 (80 regs); 8 (64 regs) spills
 #endif
     static constexpr int kMinBlocks = sizeof(W) == 4 ? 8 : MCSG_U64_MIN_BLOCKS;  // __launch_bounds__
+    // 64-bit kernel: a level whose live vertex sets fit 32 bits runs its
+    // subtree compacted (CompactSearch, nested in the task) — 97% of C4's nodes
+    static constexpr bool kNest = sizeof(W) == 8;
+    static constexpr bool kDir = DIR;
     using Set = W;
-    using Sm = WarpSmem<W, DIR>;
+    using Sm = SmT;
     using Desc = InstanceDesc;
     using Slot = TaskSlot;
     struct HParts {
@@ -314,6 +344,20 @@ struct Search {
     __device__ static __forceinline__ const Desc* descs(const KernelParams& p) { return p.inst; }
     __device__ static __forceinline__ Slot* slots(const KernelParams& p) { return p.slots; }
     __device__ static __forceinline__ int key_slot(unsigned key) { return int(key & 127u); }
+    // vertex-id hooks (identity: the 32-bit compacted policy maps ids) and
+    // the class-stack limit of the level placement
+    __device__ __forceinline__ int g_orig(int v) const { return v; }
+    __device__ __forceinline__ int h_orig(int u) const { return u; }
+    __device__ __forceinline__ int g_local(int v) const { return v; }
+    __device__ __forceinline__ int stack_limit(const KernelParams& p) const { return p.smem_classes + p.spill_classes; }
+    // the current level's live vertex sets (∪L, ∪R) fit 32 bits
+    __device__ __forceinline__ bool level_live(int nc, uint64_t& lg, uint64_t& lh) const {
+        if (nc > 32 || two) return false;
+        const uint64_t l = uint64_t(L[0]), r = uint64_t(R[0]);
+        lg = uint64_t(__reduce_or_sync(kFull, unsigned(l))) | (uint64_t(__reduce_or_sync(kFull, unsigned(l >> 32))) << 32);
+        lh = uint64_t(__reduce_or_sync(kFull, unsigned(r))) | (uint64_t(__reduce_or_sync(kFull, unsigned(r >> 32))) << 32);
+        return __popcll(lg) <= 32 && __popcll(lh) <= 32;
+    }
 
     // adjacency rows (and the parity-mode vertex keys) of a new instance
     template <bool PAR>
@@ -564,6 +608,121 @@ struct Search {
     }
 };
 
+// ------------------------------------------------------- compacted subtrees --
+// The 64-bit kernel runs a subtree whose live vertex sets fit 32 bits with
+// the 32-bit policy on renumbered vertices: compact id j is the j-th live
+// vertex (ascending original id, so every selection rule, being an order on
+// ids, picks the same vertex and class as the 64-bit policy would). Rows are
+// rebuilt for the live vertices (CompactArea), the class stack is the 64-bit
+// stack's free memory above the enclosing level, seen as 8-byte classes (at
+// most m(m+1)/2 + 32 of them for m = min(|∪L|, |∪R|)), and ids are mapped back wherever
+// they leave the subtree: offered mappings, donated subtrees (in the 64-bit
+// format, so any warp can take them).
+template <bool DIR>
+struct CompactSearch : Search<uint32_t, DIR, CompactRows<DIR>> {
+    using Base = Search<uint32_t, DIR, CompactRows<DIR>>;
+    using Set = uint32_t;
+    using Desc = InstanceDesc;
+    using Slot = TaskSlot;
+    using KSm = WarpSmem<uint64_t, DIR>;
+    static constexpr bool kNest = false;
+
+    KSm& ks;  // the kernel's (64-bit) per-warp memory: mapping prefix, maps
+
+    __device__ __forceinline__ CompactSearch(KSm& ks_, Cls<uint32_t>* scls_, int cap_, int lane_, unsigned lt_)
+        : Base(ks_.ca.img, scls_, nullptr, cap_, lane_, lt_), ks(ks_) {}
+
+    __device__ __forceinline__ int g_orig(int v) const { return ks.ca.gid[v]; }
+    __device__ __forceinline__ int h_orig(int u) const { return ks.ca.hid[u]; }
+    __device__ __forceinline__ int g_local(int v) const { return ks.ca.cmap_g[v]; }
+    __device__ __forceinline__ int stack_limit(const KernelParams&) const { return this->cap; }
+
+    // compact image of row x (⊆ the live set) through an id map
+    __device__ static __forceinline__ uint32_t compress(uint64_t x, const uint8_t* cmap) {
+        uint32_t r = 0;
+        for (uint32_t lo = uint32_t(x); lo; lo &= lo - 1) r |= 1u << cmap[__ffs(lo) - 1];
+        for (uint32_t hi = uint32_t(x >> 32); hi; hi &= hi - 1) r |= 1u << cmap[32 + __ffs(hi) - 1];
+        return r;
+    }
+
+    // Builds the compact area for live sets lg (G) and lh (H) from the
+    // instance's 64-bit rows in the kernel's shared memory. (Siblings
+    // rarely share live sets: reusing the last area hit 2% of C4's nests.)
+    __device__ __forceinline__ void build(uint64_t lg, uint64_t lh) {
+        const int lane = this->lane;
+        for (int x = lane; x < 64; x += 32) {
+            if ((lg >> x) & 1) {
+                const int j = __popcll(lg & ((1ull << x) - 1));
+                ks.ca.gid[j] = uint8_t(x);
+                ks.ca.cmap_g[x] = uint8_t(j);
+            }
+            if ((lh >> x) & 1) {
+                const int j = __popcll(lh & ((1ull << x) - 1));
+                ks.ca.hid[j] = uint8_t(x);
+                ks.ca.cmap_h[x] = uint8_t(j);
+            }
+        }
+        __syncwarp();
+        // lane j builds row j: bit k = code bit toward the k-th live vertex
+        const int ng = __popcll(lg), nh = __popcll(lh);
+        auto& img = ks.ca.img;
+        uint32_t og = 0, oh = 0, ig = 0, ih = 0;
+        if (lane < ng) {
+            const int xg = ks.ca.gid[lane];
+            og = compress(ks.out_g[xg] & lg, ks.ca.cmap_g);
+            if constexpr (DIR) ig = compress(ks.in_g[xg] & lg, ks.ca.cmap_g);
+        }
+        if (lane < nh) {
+            const int xh = ks.ca.hid[lane];
+            oh = compress(ks.out_h[xh] & lh, ks.ca.cmap_h);
+            if constexpr (DIR) ih = compress(ks.in_h[xh] & lh, ks.ca.cmap_h);
+        }
+        img.out_g[lane] = og;
+        img.out_h[lane] = oh;
+        if constexpr (DIR) {
+            img.in_g[lane] = ig;
+            img.in_h[lane] = ih;
+        }
+        __syncwarp();
+    }
+
+    __device__ __forceinline__ uint32_t pack_g(uint64_t x) const {
+        uint32_t r = 0;
+        for (; x; x &= x - 1) r |= 1u << ks.ca.cmap_g[__ffsll(x) - 1];
+        return r;
+    }
+    __device__ __forceinline__ uint32_t pack_h(uint64_t x) const {
+        uint32_t r = 0;
+        for (; x; x &= x - 1) r |= 1u << ks.ca.cmap_h[__ffsll(x) - 1];
+        return r;
+    }
+    __device__ __forceinline__ uint64_t unpack_g(uint32_t x) const {
+        uint64_t r = 0;
+        for (; x; x &= x - 1) r |= 1ull << ks.ca.gid[__ffs(x) - 1];
+        return r;
+    }
+    __device__ __forceinline__ uint64_t unpack_h(uint32_t x) const {
+        uint64_t r = 0;
+        for (; x; x &= x - 1) r |= 1ull << ks.ca.hid[__ffs(x) - 1];
+        return r;
+    }
+
+    // the enclosing 64-bit level (lane = class, registers) as the compact
+    // stack's level 0
+    __device__ __forceinline__ void put_level(uint64_t l, uint64_t r, int nc) {
+        if (this->lane < nc) this->scls[this->lane] = Cls<uint32_t>{pack_g(l), pack_h(r)};
+    }
+    __device__ __forceinline__ void store_task(Slot& sl, int fbase, int fnc) const {
+        const Cls<uint32_t>* fp = this->at(fbase);
+        for (int i = this->lane; i < fnc; i += 32) {
+            const Cls<uint32_t> c = fp[i];
+            sl.cls_l[i] = unpack_g(c.l);
+            sl.cls_r[i] = unpack_h(c.r);
+        }
+    }
+    __device__ __forceinline__ void put_cand(Slot&, TaskHeader& h, uint32_t give) const { h.cand = unpack_h(give); }
+};
+
 // ------------------------------------------------------------- wide graphs --
 // 64 < n <= 255: a bitset is NW 64-bit words (NW = 2: n <= 128, NW = 4:
 // n <= 255). A class no longer fits a lane's registers, and a level can hold
@@ -602,6 +761,7 @@ struct WideSearch {
     static constexpr int P = DIR ? 4 : 2;
     static constexpr int kMinBlocks = 2;
     static constexpr bool kSpill = true;
+    static constexpr bool kNest = false;
     struct HParts {
         Set o, i;  // H rows of u (out; in when directed)
     };
@@ -623,6 +783,12 @@ struct WideSearch {
     __device__ static __forceinline__ const Desc* descs(const KernelParams& p) { return p.winst; }
     __device__ static __forceinline__ Slot* slots(const KernelParams& p) { return p.wslots; }
     __device__ static __forceinline__ int key_slot(unsigned key) { return int(key & 255u); }
+    // vertex-id hooks (identity: the 32-bit compacted policy maps ids) and
+    // the class-stack limit of the level placement
+    __device__ __forceinline__ int g_orig(int v) const { return v; }
+    __device__ __forceinline__ int h_orig(int u) const { return u; }
+    __device__ __forceinline__ int g_local(int v) const { return v; }
+    __device__ __forceinline__ int stack_limit(const KernelParams& p) const { return p.smem_classes + p.spill_classes; }
 
     // select_label_class key: (max, min, lowest left id, slot), 8 bits each
     template <bool TOP>

@@ -32,7 +32,7 @@ out['pipes_pct'] = {k.replace('sm__inst_executed_pipe_', '').replace('.avg.pct_o
 import hashlib, os
 _h = hashlib.sha1()
 _root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1908_06418_b200", "csrc")
-for _f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_device.h"):
+for _f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_task_body.inc", "mcsg_device.h"):
     _h.update(open(os.path.join(_root, _f), "rb").read())
 out['kernel_src_sha1'] = _h.hexdigest()
 print(json.dumps(out, indent=1))
