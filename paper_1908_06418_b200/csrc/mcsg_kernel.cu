@@ -28,6 +28,11 @@
 //                from the top. The host relabels G in REVERSE (degree desc,
 //                id asc) order so select_vertex is a single FLO.
 //   RST = true   throughput mode with restarts (restart_mult > 0).
+//   X = Search<u64>, throughput, no restarts: a level whose live vertex sets
+//                fit 32 bits runs its subtree in place with the 32-bit
+//                policy on renumbered vertices (CompactSearch, run_nested).
+// The task body (select/next/cont/pop and the task's bookkeeping) is
+// mcsg_task_body.inc, included once per policy.
 #include "mcsg_search.cuh"
 
 namespace mcsg {
