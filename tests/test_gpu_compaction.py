@@ -80,3 +80,38 @@ def test_compaction_c3_and_c4():
     g, h = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
     r = M.solve(g, h, M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=120))
     assert r.status == M.SolveStatus.optimal and r.size == 16 and M.verify(g, h, r.best)
+
+
+def test_compacted_subtrees_under_heavy_donation(monkeypatch):
+    # 16-node polls: the nested 32-bit DFS donates its levels (ids mapped
+    # back to the 64-bit ring format) hundreds of thousands of times; the
+    # exhaustive tree must stay the same tree, node for node
+    monkeypatch.setenv("MCSG_DEBUG_POLL_INTERVAL", "16")
+    for n, p, s, directed, labels in [(40, 0.4, 21, False, 16), (40, 0.2, 77, False, 12), (36, 0.5, 9, True, 12)]:
+        g, h, go, ho = pair(n, p, s, directed, labels)
+        on = _exhaustive(g, h)
+        monkeypatch.setenv("MCSG_DEBUG_NO_COMPACT", "1")
+        off = _exhaustive(g, h)
+        monkeypatch.delenv("MCSG_DEBUG_NO_COMPACT")
+        assert on.status == off.status == M.SolveStatus.optimal
+        assert on.size == off.size and on.stats.recursions == off.stats.recursions, (n, p, s)
+        assert M.verify(g, h, on.best)
+    # and C3-style directed labelled pairs, pruning on: the same optima as
+    # without compaction
+    pairs = []
+    i = 0
+    for L in (2, 4, 8):
+        for p in (0.1, 0.3, 0.5):
+            for _ in range(2):
+                pairs.append((M.random_graph(40, p, 40000 + 2 * i, True, L),
+                              M.random_graph(40, p, 40001 + 2 * i, True, L)))
+                i += 1
+    on, st = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    monkeypatch.setenv("MCSG_DEBUG_NO_COMPACT", "1")
+    off, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    monkeypatch.delenv("MCSG_DEBUG_NO_COMPACT")
+    assert [r.size for r in on] == [r.size for r in off]
+    assert all(r.status == M.SolveStatus.optimal for r in on)
+    assert st.donations > 10000
+    for (g, h), r in zip(pairs, on):
+        assert M.verify(g, h, r.best)
