@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define MCSG_ABI_VERSION 3
+#define MCSG_ABI_VERSION 4
 
 /* status codes (mirror mcs_main.cpp:22-24 exit codes; SolveStatus solve.hpp:23) */
 #define MCSG_OPTIMAL 0
@@ -107,6 +107,13 @@ typedef struct mcsg_options {
      * into the task ring and resumes with the oldest queued subtree — the
      * search stays complete. 0 = off. */
     double restart_multiplier;
+    /* SolveConfig::shared_bound (SharedBound, solve.hpp:70-81), live: may be
+     * NULL. While the call runs the host mirrors *shared_bound into the
+     * kernel, which folds it into its prune threshold at every poll (a size
+     * floor raised by other engines mid-run), and raises *shared_bound
+     * (atomic max) to the size of every mapping the search stores. floor_size
+     * is the same floor fixed at call start. */
+    volatile int32_t* shared_bound;
 } mcsg_options;
 
 #define MCSG_JUMP_PLUS_ONE 1
@@ -135,6 +142,9 @@ typedef struct mcsg_stats {
     uint64_t idle_cycles;    /* Σ over warps of SM cycles waiting for a task */
     uint64_t restarts;       /* restart events (group 0 of the call) */
     uint64_t frozen;         /* subtrees frozen into the ring by restarts */
+    double idle_s;           /* idle_cycles / the device's SM clock (SearchStats::idle_seconds) */
+    double busy_s;           /* busy_cycles / the device's SM clock */
+    uint64_t peer_pushes;    /* incumbent improvements pushed to peer GPUs over NVLink P2P */
 } mcsg_stats;
 
 typedef struct mcsg_result {

@@ -56,23 +56,33 @@ inline mcsg_options to_options(const SolveConfig& cfg, int mode) {
     o.mode = mode;
     o.disable_pruning = cfg.disable_pruning ? 1 : 0;
     o.floor_size = cfg.shared_bound ? static_cast<int32_t>(cfg.shared_bound->get()) : 0;
+    o.shared_bound = nullptr;  // set by CancelBridge when cfg.shared_bound is given
     o.device = -1;
     o.cancel = nullptr;  // set by CancelBridge when cfg.cancel is given
     return o;
 }
 
-// SolveConfig::cancel is a std::atomic<bool>; the ABI polls an int32. A small
-// watcher thread mirrors one into the other for the duration of a call.
+// SolveConfig::cancel is a std::atomic<bool> and SolveConfig::shared_bound a
+// SharedBound (atomic long long); the ABI polls int32s. A small watcher thread
+// mirrors them for the duration of a call: the cancel flag and the bound's
+// rises in, the kernel's stored improvements out (SharedBound::bump), so a
+// GPU member of a CPU portfolio sees and feeds mid-run improvements.
 class CancelBridge {
 public:
-    CancelBridge(const std::atomic<bool>* src, mcsg_options& o) : src_(src) {
-        if (!src_) return;
-        o.cancel = &flag_;
+    CancelBridge(const std::atomic<bool>* src, mcsg_options& o, SharedBound* bound = nullptr)
+        : src_(src), bound_(bound) {
+        if (!src_ && !bound_) return;
+        if (src_) o.cancel = &flag_;
+        if (bound_) {
+            shared_ = static_cast<int32_t>(bound_->get());
+            o.shared_bound = &shared_;
+        }
         watcher_ = std::thread([this] {
             while (!done_.load()) {
-                if (src_->load()) flag_ = 1;
+                sync();
                 std::this_thread::sleep_for(std::chrono::microseconds(200));
             }
+            sync();
         });
     }
     ~CancelBridge() {
@@ -81,8 +91,22 @@ public:
     }
 
 private:
+    void sync() {
+        if (src_ && src_->load()) flag_ = 1;
+        if (!bound_) return;
+        const int32_t mine = __atomic_load_n(&shared_, __ATOMIC_ACQUIRE);
+        bound_->bump(mine);  // the kernel's improvements out
+        const long long ext = bound_->get();
+        int32_t cur = mine;  // other engines' rises in (atomic max: the library writes too)
+        while (ext > cur && !__atomic_compare_exchange_n(&shared_, &cur, static_cast<int32_t>(ext), true,
+                                                         __ATOMIC_RELEASE, __ATOMIC_ACQUIRE)) {
+        }
+    }
+
     const std::atomic<bool>* src_;
+    SharedBound* bound_;
     volatile int32_t flag_ = 0;
+    volatile int32_t shared_ = 0;
     std::atomic<bool> done_{false};
     std::thread watcher_;
 };
@@ -98,7 +122,7 @@ inline SolveResult to_result(const mcsg_result& r, const mcsg_stats& st) {
     out.stats.wall_seconds = st.wall_s;
     out.stats.probes = st.probes;
     out.stats.tasks_published = st.donations;                    // subtrees handed to idle warps
-    out.stats.idle_seconds = double(st.idle_cycles) / 1.965e9;  // Σ warps' wait for work (B200 SM clock)
+    out.stats.idle_seconds = st.idle_s;  // Σ warps' wait for work (cycles / the device's SM clock)
     out.stats.deadend_suspects = (r.flags & MCSG_RESULT_SUSPECT) ? 1 : 0;
     if (out.status == SolveStatus::optimal) out.stats.visited_ranges = 1;  // the whole tree, exactly once
     return out;
@@ -114,11 +138,10 @@ inline SolveResult solve(const Graph& g, const Graph& h, const SolveConfig& cfg 
                          int mode = MCSG_MODE_THROUGHPUT) {
     GraphBuffer gb(g), hb(h);
     mcsg_options o = to_options(cfg, mode);
-    CancelBridge bridge(cfg.cancel, o);
+    CancelBridge bridge(cfg.cancel, o, cfg.shared_bound);
     mcsg_result r{};
     mcsg_stats st{};
     check(mcsg_solve(&gb.view, &hb.view, &o, &r, &st));
-    if (cfg.shared_bound) cfg.shared_bound->bump(r.size);
     return to_result(r, st);
 }
 
@@ -126,7 +149,7 @@ inline SolveResult solve(const Graph& g, const Graph& h, const SolveConfig& cfg 
 inline SolveResult solve_goal_directed(const Graph& g, const Graph& h, const SolveConfig& cfg = {}) {
     GraphBuffer gb(g), hb(h);
     mcsg_options o = to_options(cfg, MCSG_MODE_THROUGHPUT);
-    CancelBridge bridge(cfg.cancel, o);
+    CancelBridge bridge(cfg.cancel, o, cfg.shared_bound);
     mcsg_result r{};
     mcsg_stats st{};
     check(mcsg_solve_goal_directed(&gb.view, &hb.view, &o, &r, &st));
@@ -138,7 +161,7 @@ inline SolveResult bound_jump_search(const Graph& g, const Graph& h, int current
                                      const SolveConfig& cfg = {}) {
     GraphBuffer gb(g), hb(h);
     mcsg_options o = to_options(cfg, MCSG_MODE_THROUGHPUT);
-    CancelBridge bridge(cfg.cancel, o);
+    CancelBridge bridge(cfg.cancel, o, cfg.shared_bound);
     mcsg_result r{};
     mcsg_stats st{};
     check(mcsg_bound_jump(&gb.view, &hb.view, current_best, mode == JumpMode::doubling ? 1 : 0, &o,

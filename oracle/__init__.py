@@ -143,6 +143,9 @@ def ref_lib():
                                            C.c_double, P(_RefResult)]
         lib.ref_bound_jump.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_int, C.c_int, C.c_double,
                                        P(_RefResult)]
+        lib.ref_solve_floor.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_int, C.c_double, P(_RefResult)]
+        lib.ref_solve_parallel_floor.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_int, C.c_int,
+                                                 C.c_double, C.c_int, P(_RefResult)]
         lib.ref_verify.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32), C.c_int]
         lib.ref_bruteforce.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32)]
         lib.ref_ordering.argtypes = [P(_OrcGraph), C.c_int, P(C.c_int32)]
@@ -293,6 +296,23 @@ def ref_solve_parallel(g: G, h: G, workers=0, part_level=5, budget=1e9) -> Resul
     r = _RefResult()
     gs, hs = g.c_struct(), h.c_struct()
     ref_lib().ref_solve_parallel(C.byref(gs), C.byref(hs), workers, part_level, budget, C.byref(r))
+    return _ref_res(r)
+
+
+def ref_solve_floor(g: G, h: G, floor: int, budget=1e9) -> Result:
+    """solve() with SolveConfig::shared_bound seeded at `floor` (search_core.hpp:21-36)."""
+    r = _RefResult()
+    gs, hs = g.c_struct(), h.c_struct()
+    ref_lib().ref_solve_floor(C.byref(gs), C.byref(hs), floor, budget, C.byref(r))
+    return _ref_res(r)
+
+
+def ref_solve_parallel_floor(g: G, h: G, floor: int, workers=0, part_level=5, budget=1e9) -> Result:
+    """solve_parallel with SolveConfig::shared_bound seeded at `floor` (solve.hpp:70-81)."""
+    r = _RefResult()
+    gs, hs = g.c_struct(), h.c_struct()
+    ref_lib().ref_solve_parallel_floor(C.byref(gs), C.byref(hs), workers, part_level, budget, floor,
+                                       C.byref(r))
     return _ref_res(r)
 
 

@@ -8,7 +8,7 @@
 //   mcs::random_graph            proj/include/mcs/graph.hpp:99
 //   mcs::parse_engine_spec       proj/include/mcs/portfolio.hpp:34
 //   mcs::run_engine              proj/include/mcs/portfolio.hpp:37
-//   mcs::solve_parallel          proj/include/mcs/engine_parallel.hpp:16
+//   mcs::solve_parallel          proj/include/mcs/engine_parallel.hpp:16 (optionally with a SharedBound floor)
 //   mcs::oracle::verify          proj/include/mcs/oracle.hpp:16
 //   mcs::oracle::mcs_bruteforce  proj/include/mcs/oracle.hpp:26
 //   mcs::make_ordering           proj/include/mcs/heuristics.hpp:26
@@ -161,6 +161,47 @@ int ref_solve_parallel(const ref_graph* g, const ref_graph* h, int workers, int 
         pc.part_level = part_level;
         pc.base.budget_seconds = budget;
         fill(mcs::solve_parallel(gg, hh, pc), out);
+        return 0;
+    } catch (const std::exception& e) {
+        fail(out, e.what());
+        return -1;
+    }
+}
+
+// Thread-pool engine seeded with an external size floor: SolveConfig::shared_bound
+// (solve.hpp:70-81,124) starts at `floor`, and the pool prunes every node whose
+// bound is <= max(incumbent, floor) (engine_parallel.cpp:75-78). Status optimal
+// with floor k therefore proves that no common subgraph larger than k exists.
+int ref_solve_parallel_floor(const ref_graph* g, const ref_graph* h, int workers, int part_level,
+                             double budget, int floor, ref_result* out) {
+    try {
+        mcs::Graph gg = to_graph(g), hh = to_graph(h);
+        mcs::SharedBound sb;
+        sb.bump(floor);
+        mcs::ParallelConfig pc;
+        pc.workers = workers;
+        pc.part_level = part_level;
+        pc.base.budget_seconds = budget;
+        pc.base.shared_bound = &sb;
+        fill(mcs::solve_parallel(gg, hh, pc), out);
+        return 0;
+    } catch (const std::exception& e) {
+        fail(out, e.what());
+        return -1;
+    }
+}
+
+// Sequential solve (solve.hpp:128) with SolveConfig::shared_bound seeded at
+// `floor`: the size-floor semantics of LocalIncumbent (search_core.hpp:21-36).
+int ref_solve_floor(const ref_graph* g, const ref_graph* h, int floor, double budget, ref_result* out) {
+    try {
+        mcs::Graph gg = to_graph(g), hh = to_graph(h);
+        mcs::SharedBound sb;
+        sb.bump(floor);
+        mcs::SolveConfig cfg;
+        cfg.budget_seconds = budget;
+        cfg.shared_bound = &sb;
+        fill(mcs::solve(gg, hh, cfg), out);
         return 0;
     } catch (const std::exception& e) {
         fail(out, e.what());

@@ -98,7 +98,7 @@ class _Options(C.Structure):
                 ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32)),
                 ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32),
                 ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32),
-                ("restart_multiplier", C.c_double)]
+                ("restart_multiplier", C.c_double), ("shared_bound", C.POINTER(C.c_int32))]
 
 
 class _Stats(C.Structure):
@@ -109,7 +109,8 @@ class _Stats(C.Structure):
                 ("ctas", C.c_int32), ("smem_per_cta", C.c_int32), ("smem_classes", C.c_int32),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64),
                 ("busy_cycles", C.c_uint64), ("idle_cycles", C.c_uint64),
-                ("restarts", C.c_uint64), ("frozen", C.c_uint64)]
+                ("restarts", C.c_uint64), ("frozen", C.c_uint64), ("idle_s", C.c_double),
+                ("busy_s", C.c_double), ("peer_pushes", C.c_uint64)]
 
 
 class _Result(C.Structure):
@@ -375,6 +376,22 @@ def verify(g: Graph, h: Graph, mapping) -> bool:
 
 
 # ------------------------------------------------------------------ solving --
+class SharedBound:
+    """SharedBound (solve.hpp:70-81): a monotone size shared between engines.
+    Passed as SolveConfig.shared_bound, the running kernel reads it as a live
+    size floor and raises it to the size of every mapping it stores."""
+
+    def __init__(self, size: int = 0):
+        self._v = C.c_int32(int(size))
+
+    def get(self) -> int:
+        return int(self._v.value)
+
+    def bump(self, size: int) -> None:
+        if size > self._v.value:
+            self._v.value = int(size)
+
+
 @dataclass
 class SolveConfig:
     """SolveConfig (solve.hpp:118-125) plus the GPU engine knobs."""
@@ -382,7 +399,7 @@ class SolveConfig:
     order: OrderingStrategy = OrderingStrategy.none
     cancel: object = None              # a ctypes c_int32 (or anything with .value) polled while running
     disable_pruning: bool = False
-    shared_bound: int = 0              # size floor (SharedBound value)
+    shared_bound: "int | SharedBound" = 0  # size floor, or a live SharedBound shared with other engines
     mode: int = MODE_THROUGHPUT        # MODE_PARITY: reference node order and counts
     device: int = -1
     max_warps: int = 0
@@ -437,6 +454,7 @@ class SearchStats:
     launches: int = 0
     busy_cycles: int = 0
     idle_cycles: int = 0
+    peer_pushes: int = 0               # incumbent sizes pushed to peer GPUs (NVLink P2P)
 
 
 @dataclass
@@ -460,7 +478,11 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
     o.mode = cfg.mode
     o.goal = 0
     o.disable_pruning = int(cfg.disable_pruning)
-    o.floor_size = int(cfg.shared_bound)
+    if isinstance(cfg.shared_bound, SharedBound):
+        o.floor_size = cfg.shared_bound.get()
+        o.shared_bound = C.pointer(cfg.shared_bound._v)
+    else:
+        o.floor_size = int(cfg.shared_bound)
     o.device = cfg.device
     o.max_warps = cfg.max_warps
     o.smem_classes = cfg.smem_classes
@@ -505,13 +527,12 @@ def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
         s.busy_cycles, s.idle_cycles = int(st.busy_cycles), int(st.idle_cycles)
         s.tasks_published = s.donations
         s.restarts, s.frozen = int(st.restarts), int(st.frozen)
-        s.idle_seconds = s.idle_cycles / _SM_HZ
+        s.peer_pushes = int(st.peer_pushes)
+        s.idle_seconds = float(st.idle_s)
     if r.status == 0:
         s.visited_ranges = 1
     return SolveResult(SolveStatus(r.status), pairs, int(r.size), s)
 
-
-_SM_HZ = 1.965e9  # B200 SM clock (MEASURED_PEAKS.json sm_max_mhz): idle cycles -> seconds
 
 
 def _check(rc: int):

@@ -150,6 +150,7 @@ struct Counters {
     unsigned long long stall_pos, stall_head, stall_tail, stall_seq;  // its ticket and the ring state
     unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
     unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks
+    unsigned long long peer_pushes;  // improvements pushed to peer devices over NVLink P2P
 };
 
 // Control words of one launch, one 128-byte line each so that idle warps
@@ -160,12 +161,19 @@ struct alignas(128) Line64 {
 struct alignas(128) Line32 {
     int32_t v;
 };
+// The stop line also carries the live external size floor (SharedBound,
+// solve.hpp:70-81): every poll prefetches the line, so the floor reaches every
+// warp with the stop word at no extra load.
+struct alignas(128) StopLine {
+    int32_t v;
+    int32_t floor;  // raised by warp 0 from the host-mapped shared bound
+};
 struct Ctl {
     Line64 head;       // ring consumer ticket
     Line64 tail;       // ring producer ticket
     Line32 pending;    // tasks queued + tasks in flight (termination)
     Line32 idle;       // warps waiting for work (donation trigger)
-    Line32 stop;       // 0 run, 1 timeout, 2 cancelled, 3 internal error
+    StopLine stop;     // 0 run, 1 timeout, 2 cancelled, 3 internal error; + live floor
     Line32 next_root;  // root tasks are implicit: instance ids handed out by atomicAdd
     Line32 live;       // instances with unfinished tasks (fairness share)
 };
@@ -191,6 +199,12 @@ struct KernelParams {
     int32_t n_peers;
     int32_t peer_done_on_complete;  // portfolio: the first device to finish proves for all
     const volatile int32_t* cancel;  // host-mapped cancel flag (may be null)
+    // Live SharedBound (solve.hpp:70-81; may be null): warp 0 reads the
+    // host-mapped size at its polls and raises ctl->stop.floor, which every
+    // warp folds into its prune threshold (never into offers); every stored
+    // improvement is pushed back to the host with a system-scope atomicMax.
+    const volatile int32_t* ext_floor;
+    int32_t* ext_best;
     unsigned long long budget_ns;    // per-warp deadline = warp start + budget, 0 = none
     uint64_t* spill;         // per-warp HBM spill area for class levels (64-bit and wide kernels)
     int32_t spill_classes;   // classes per warp in the spill area

@@ -84,6 +84,11 @@ struct Context {
     size_t spill_bytes = 0;
     int32_t* h_cancel = nullptr;  // pinned, mapped
     int32_t* d_cancel = nullptr;
+    int32_t* h_xfloor = nullptr;  // live SharedBound: host -> kernel (pinned, mapped)
+    int32_t* d_xfloor = nullptr;
+    int32_t* h_xbest = nullptr;   // stored improvements: kernel -> host (pinned, mapped)
+    int32_t* d_xbest = nullptr;
+    int clock_khz = 0;            // SM clock (cycle counters -> seconds)
     std::mutex mu;
 
     explicit Context(int dev) : device(dev) {
@@ -106,6 +111,12 @@ struct Context {
         ck(cudaHostAlloc(&h_cancel, sizeof(int32_t), cudaHostAllocMapped), "cancel flag");
         ck(cudaHostGetDevicePointer(&d_cancel, h_cancel, 0), "cancel flag map");
         *h_cancel = 0;
+        ck(cudaHostAlloc(&h_xfloor, sizeof(int32_t), cudaHostAllocMapped), "shared bound");
+        ck(cudaHostGetDevicePointer(&d_xfloor, h_xfloor, 0), "shared bound map");
+        ck(cudaHostAlloc(&h_xbest, sizeof(int32_t), cudaHostAllocMapped), "shared bound");
+        ck(cudaHostGetDevicePointer(&d_xbest, h_xbest, 0), "shared bound map");
+        *h_xfloor = *h_xbest = 0;
+        ck(cudaDeviceGetAttribute(&clock_khz, cudaDevAttrClockRate, dev), "clock rate");
     }
 
     void reserve(size_t n_inst, size_t n_grp, size_t spill) {
@@ -213,6 +224,7 @@ struct LaunchOut {
     double kernel_s = 0, h2d_s = 0;
     int warps = 0, ctas = 0, smem_per_cta = 0, smem_classes = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
+    int clock_khz = 0;
 };
 
 Job make_job(const HostGraph& g, const HostGraph& h, int order) {
@@ -268,6 +280,13 @@ void relabel_for_throughput(Job& j, uint64_t seed = 0) {
         for (int u = 0; u < m; ++u) ih[ph[u]] = j.inv_h.empty() ? u : j.inv_h[u];
         j.h = j.h.permuted(ph);
         j.inv_h = std::move(ih);
+    }
+}
+
+// SharedBound::bump (solve.hpp:73-77) on the caller's int32
+void bump_shared(volatile int32_t* sb, int32_t size) {
+    int32_t cur = __atomic_load_n(sb, __ATOMIC_ACQUIRE);
+    while (size > cur && !__atomic_compare_exchange_n(sb, &cur, size, true, __ATOMIC_RELEASE, __ATOMIC_ACQUIRE)) {
     }
 }
 
@@ -428,6 +447,8 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     }
     f.seeded = n_seeded;
     *ctx.h_cancel = 0;
+    *ctx.h_xbest = 0;
+    *ctx.h_xfloor = o.shared_bound ? std::max(0, int(*o.shared_bound)) : 0;
 
     KernelParams p{};
     p.inst = ctx.d_inst;
@@ -461,6 +482,8 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     for (int q = 0; q < p.n_peers; ++q) p.peer_grp[q] = ex.peers[q];
     p.peer_done_on_complete = ex.peer_done_on_complete ? 1 : 0;
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
+    p.ext_floor = o.shared_bound ? ctx.d_xfloor : nullptr;
+    p.ext_best = o.shared_bound ? ctx.d_xbest : nullptr;
     p.budget_ns = o.budget_s >= 1e8 ? 0ull : (unsigned long long)(o.budget_s * 1e9);
     p.spill = ctx.d_spill;
     p.spill_classes = f.spill_classes;
@@ -497,14 +520,23 @@ LaunchOut finish(InFlight& f) {
     const int n = f.n, n_groups = f.n_groups;
     out.jobs.resize(n);
     out.groups.resize(n_groups);
-    if (f.o.cancel) {
-        // mirror the caller's flag into host-mapped memory the kernel polls
+    if (f.o.cancel || f.o.shared_bound) {
+        // mirror the caller's cancel flag and SharedBound into host-mapped
+        // memory the kernel polls, and the kernel's stored improvements back
+        volatile int32_t* xf = ctx.h_xfloor;
+        volatile int32_t* xb = ctx.h_xbest;
         while (cudaStreamQuery(ctx.stream) == cudaErrorNotReady) {
-            if (*f.o.cancel) *reinterpret_cast<volatile int32_t*>(ctx.h_cancel) = 1;
+            if (f.o.cancel && *f.o.cancel) *reinterpret_cast<volatile int32_t*>(ctx.h_cancel) = 1;
+            if (f.o.shared_bound) {
+                const int32_t ext = *f.o.shared_bound;
+                if (ext > *xf) *xf = ext;
+                bump_shared(f.o.shared_bound, *xb);
+            }
             std::this_thread::sleep_for(std::chrono::microseconds(50));
         }
     }
     ck(cudaStreamSynchronize(ctx.stream), "search kernel");
+    if (f.o.shared_bound) bump_shared(f.o.shared_bound, *reinterpret_cast<volatile int32_t*>(ctx.h_xbest));
     float ms = 0;
     cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1);
     out.kernel_s = ms * 1e-3;
@@ -512,6 +544,7 @@ LaunchOut finish(InFlight& f) {
     out.counters = *ctx.h_cnt;
     out.warps = f.warps;
     out.ctas = f.ctas;
+    out.clock_khz = ctx.clock_khz;
     out.smem_per_cta = kernel_smem_per_warp(f.bits, f.directed, f.smem_classes) * kWarpsPerCta;
     out.smem_classes = f.smem_classes;
     out.h2d_bytes = ((f.bits > 64 ? sizeof(WideDesc) : sizeof(InstanceDesc)) + sizeof(InstanceState)) * uint64_t(n) +
@@ -703,7 +736,9 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
         const JobResult& r = lo.jobs[0];
         nodes += r.nodes;
         all_complete &= r.completed;
-        any_done_max |= lo.groups[0].done && !r.completed;  // stopped early because the max was reached
+        // stopped early because the max (or a probe goal) was reached; a
+        // dead-end suspect verdict also raises done but proves nothing
+        any_done_max |= lo.groups[0].done && !lo.groups[0].suspect && !r.completed;
         if (r.size > best.size) best = r;
         if (r.status != MCSG_OPTIMAL) status = r.status;
         best.solve_s = std::max(best.solve_s, r.solve_s);
@@ -721,6 +756,7 @@ JobResult solve_sharded(const HostGraph& G, const HostGraph& H, const mcsg_optio
         agg->counters.tasks += outs[i].counters.tasks;
         agg->counters.busy_cycles += outs[i].counters.busy_cycles;
         agg->counters.idle_cycles += outs[i].counters.idle_cycles;
+        agg->counters.peer_pushes += outs[i].counters.peer_pushes;
         agg->warps += outs[i].warps;
         agg->ctas += outs[i].ctas;
         agg->h2d_bytes += outs[i].h2d_bytes;
@@ -755,6 +791,10 @@ void fill_stats(mcsg_stats* st, const LaunchOut& lo, double wall, uint64_t probe
     st->idle_cycles = lo.counters.idle_cycles;
     st->restarts = lo.groups.empty() ? 0 : lo.groups[0].restarts;
     st->frozen = lo.counters.frozen;
+    const double hz = lo.clock_khz > 0 ? lo.clock_khz * 1e3 : 1.0;
+    st->idle_s = double(lo.counters.idle_cycles) / hz;
+    st->busy_s = double(lo.counters.busy_cycles) / hz;
+    st->peer_pushes = lo.counters.peer_pushes;
     if (std::getenv("MCSG_DEBUG_NESTS"))
         std::fprintf(stderr, "nests smem %llu hbm %llu\n", lo.counters.nests_smem, lo.counters.nests_hbm);
 }
@@ -781,6 +821,10 @@ void accumulate(mcsg_stats* st, const LaunchOut& lo) {
     st->idle_cycles += lo.counters.idle_cycles;
     st->restarts += lo.groups.empty() ? 0 : lo.groups[0].restarts;
     st->frozen += lo.counters.frozen;
+    const double hz = lo.clock_khz > 0 ? lo.clock_khz * 1e3 : 1.0;
+    st->idle_s += double(lo.counters.idle_cycles) / hz;
+    st->busy_s += double(lo.counters.busy_cycles) / hz;
+    st->peer_pushes += lo.counters.peer_pushes;
 }
 
 mcsg_options defaults(const mcsg_options* o) {
@@ -917,14 +961,40 @@ int32_t mcsg_solve_batch(int32_t count, const mcsg_graph* gs, const mcsg_graph* 
     }
 }
 
+// mcs::solve on one device (a batch of one) or sharded over o.n_devices.
+static int32_t solve_plain(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options& o, mcsg_result* out,
+                           mcsg_stats* stats) {
+    if (o.n_devices <= 1) return mcsg_solve_batch(1, g, h, &o, out, stats);
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (o.n_devices > 16) throw Error("at most 16 devices");
+        if (o.mode == MCSG_MODE_PARITY) throw Error("parity mode runs on one device");
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        LaunchOut agg;
+        uint64_t host_nodes = 0;
+        const JobResult r = solve_sharded(G, H, o, &agg, &host_nodes);
+        write_result(G, H, r, out);
+        fill_stats(stats, agg, secs_since(t0), 0);
+        if (stats) stats->nodes += host_nodes;
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
                    mcsg_result* out, mcsg_stats* stats) {
     const mcsg_options o = defaults(opt);
-    if (o.n_devices <= 1 && o.deadend_jump != 0 && (o.deadend_abs || o.deadend_rel > 0)) {
+    if (o.deadend_jump != 0 && (o.deadend_abs || o.deadend_rel > 0)) {
         // forecast-then-mitigate (portfolio.cpp:136-155): monitored solve; on a
         // suspect verdict the bound jump resumes from the incumbent size
         const auto t0 = std::chrono::steady_clock::now();
-        const int32_t rc = mcsg_solve_batch(1, g, h, &o, out, stats);
+        const int32_t rc = solve_plain(g, h, o, out, stats);
         if (rc == MCSG_ERROR || !(out->flags & MCSG_RESULT_SUSPECT)) return rc;
         mcsg_options rest = o;
         rest.deadend_jump = 0;
@@ -952,27 +1022,7 @@ int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options*
         }
         return out->status;
     }
-    if (o.n_devices <= 1) return mcsg_solve_batch(1, g, h, opt, out, stats);
-    try {
-        const auto t0 = std::chrono::steady_clock::now();
-        if (o.n_devices > 16) throw Error("at most 16 devices");
-        if (o.mode == MCSG_MODE_PARITY) throw Error("parity mode runs on one device");
-        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
-        check_pair(G, H);
-        if (o.budget_s <= 0) {
-            timed_out(out);
-            return MCSG_TIMEOUT;
-        }
-        LaunchOut agg;
-        uint64_t host_nodes = 0;
-        const JobResult r = solve_sharded(G, H, o, &agg, &host_nodes);
-        write_result(G, H, r, out);
-        fill_stats(stats, agg, secs_since(t0), 0);
-        if (stats) stats->nodes += host_nodes;
-        return out->status;
-    } catch (const std::exception& e) {
-        return fail(e);
-    }
+    return solve_plain(g, h, o, out, stats);
 }
 
 int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
@@ -1005,6 +1055,12 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
         }
         mcsg_options lo_opt = o;
         lo_opt.mode = MCSG_MODE_THROUGHPUT;  // members share the incumbent size
+        // dead-end handling belongs to a member's engine spec (run_engine,
+        // portfolio.cpp:136-155), never to the race: a suspect verdict would
+        // stop every member without proving anything
+        lo_opt.deadend_abs = 0;
+        lo_opt.deadend_rel = 0;
+        lo_opt.deadend_jump = 0;
         std::vector<JobResult> members(count);
         bool done = false;
         int w = -1;
@@ -1012,7 +1068,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
         if (o.n_devices <= 1) {
             lo = launch(jobs, 1, lo_opt);
             members = lo.jobs;
-            done = lo.groups[0].done;
+            done = lo.groups[0].done && !lo.groups[0].suspect;
             w = lo.groups[0].winner;
         } else {
             // members spread over the devices; the first to finish stops all (P2P done flag)
@@ -1034,7 +1090,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
             double first = 1e300;
             for (size_t d = 0; d < outs.size(); ++d) {
                 for (size_t k = 0; k < used_index[d].size(); ++k) members[used_index[d][k]] = outs[d].jobs[k];
-                if (outs[d].groups[0].done) {
+                if (outs[d].groups[0].done && !outs[d].groups[0].suspect) {
                     done = true;
                     const int lw = outs[d].groups[0].winner;
                     if (lw >= 0 && outs[d].jobs[lw].completed && outs[d].jobs[lw].solve_s < first) {
@@ -1046,6 +1102,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
             lo = outs[0];
             for (size_t d = 1; d < outs.size(); ++d) {
                 lo.counters.nodes += outs[d].counters.nodes;
+                lo.counters.peer_pushes += outs[d].counters.peer_pushes;
                 lo.kernel_s = std::max(lo.kernel_s, outs[d].kernel_s);
                 lo.warps += outs[d].warps;
                 lo.launches += outs[d].launches;
@@ -1115,9 +1172,9 @@ int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
         }
         if (swapped) std::swap(G, H);
         write_result(G, H, r, out);
+        out->probes = int32_t(probes);
         if (stats) {
             stats->probes = probes;
-            out->probes = int32_t(probes);
             stats->wall_s = secs_since(t0);
         }
         return out->status;
@@ -1189,9 +1246,9 @@ int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t curren
             if (!base.inv_h.empty()) r.pairs[2 * k + 1] = base.inv_h[r.pairs[2 * k + 1]];
         }
         write_result(G, H, r, out);
+        out->probes = int32_t(probes);
         if (stats) {
             stats->probes = probes;
-            out->probes = int32_t(probes);
             stats->wall_s = secs_since(t0);
         }
         return out->status;

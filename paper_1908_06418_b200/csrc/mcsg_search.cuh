@@ -615,7 +615,8 @@ struct Search {
 // ids, picks the same vertex and class as the 64-bit policy would). Rows are
 // rebuilt for the live vertices (CompactArea), the class stack is the 64-bit
 // stack's free memory above the enclosing level, seen as 8-byte classes (at
-// most m(m+1)/2 + 32 of them for m = min(|∪L|, |∪R|)), and ids are mapped back wherever
+// most nc + m(m-1)/2 + 32 of them for m = min(|∪L|, |∪R|) and the enclosing
+// level's nc entries, dead ones included), and ids are mapped back wherever
 // they leave the subtree: offered mappings, donated subtrees (in the 64-bit
 // format, so any warp can take them).
 template <bool DIR>

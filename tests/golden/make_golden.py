@@ -4,7 +4,7 @@ Runs in the dev container only (needs oracle/_ref/libmcs_ref.so, built from
 /root/reference/proj/src by oracle/Makefile). The JSON fixtures it writes are
 committed; tests on the GPU box read them without the reference.
 
-    python tests/golden/make_golden.py [small|c2|c5|c3|all]
+    python tests/golden/make_golden.py [small|c2|c5|c3|all|c5full|c4]
 """
 from __future__ import annotations
 
@@ -169,6 +169,105 @@ def c5(count=300):
     dump("c5_sample.json", out)
 
 
+def floor():
+    """Size-floor semantics (SolveConfig::shared_bound, search_core.hpp:21-36):
+    sequential solve() with floors below, at and above the optimum."""
+    out = []
+    for n, d, s in random_pairs(24, 8, 20, 7070):
+        g, h = O.ref_random_graph(n, d, s), O.ref_random_graph(n, d, s + 1)
+        opt = O.ref_run_engine(g, h, "recursive").size
+        for f in sorted({0, max(opt - 2, 0), max(opt - 1, 0), opt, opt + 1}):
+            r = O.ref_solve_floor(g, h, f)
+            out.append({"n": n, "d": d, "seed": s, "floor": f, "opt": opt, "status": r.status, "size": r.size,
+                        "nodes": r.nodes, "pairs": [list(p) for p in r.pairs]})
+    dump("floor.json", {"cases": out})
+
+
+def c3_pairs():
+    """C3 (BASELINE configs[2]): directed vertex-labelled ER n=40,
+    L in {2,4,8} x p in {.1,.3,.5} x 10 pairs, seeds 40000+2i / 40001+2i."""
+    out = []
+    i = 0
+    for L in (2, 4, 8):
+        for p in (0.1, 0.3, 0.5):
+            for _ in range(10):
+                out.append((i, L, p))
+                i += 1
+    return out
+
+
+def _c3_one(args):
+    i, L, p = args
+    g = O.ref_random_graph(40, p, 40000 + 2 * i, True, L)
+    h = O.ref_random_graph(40, p, 40001 + 2 * i, True, L)
+    t0 = time.time()
+    r = O.ref_solve_parallel(g, h, workers=2, part_level=5, budget=7200)
+    return i, L, p, r.status, r.size, r.nodes, time.time() - t0
+
+
+def c3():
+    out = {"pairs": [], "how": "reference solve_parallel(workers=2, part_level=5) per pair, 4 pairs at a time"}
+    with ProcessPoolExecutor(4) as ex:
+        for i, L, p, st, sz, nodes, secs in ex.map(_c3_one, c3_pairs()):
+            out["pairs"].append({"i": i, "labels": L, "p": p, "status": st, "size": sz,
+                                 "pool_nodes": nodes, "pool_seconds": round(secs, 3)})
+            print("c3", i, L, p, st, sz, nodes, round(secs, 2), flush=True)
+    assert all(r["status"] == 0 for r in out["pairs"])
+    dump("c3_sizes.json", out)
+
+
+def _c5_full_one(i):
+    n = 16 + (i // 3) % 9
+    p = (0.1, 0.3, 0.5)[i % 3]
+    g, h = O.ref_random_graph(n, p, 50000 + 2 * i), O.ref_random_graph(n, p, 50001 + 2 * i)
+    r = O.ref_run_engine(g, h, "recursive", 120)
+    eng = "recursive"
+    if r.status != 0:  # the rare long pair: the reference pool proves it
+        r = O.ref_solve_parallel(g, h, workers=2, part_level=5, budget=7200)
+        eng = "parallel:2"
+    return i, r.status, r.size, r.nodes, eng
+
+
+def c5_full(count=10000):
+    """All 10,000 C5 optima; compact form (sizes as one string of bytes)."""
+    sizes = [0] * count
+    nodes = [0] * count
+    eng = {}
+    with ProcessPoolExecutor(8) as ex:
+        for i, st, sz, nd, e in ex.map(_c5_full_one, range(count), chunksize=16):
+            assert st == 0, (i, st)
+            sizes[i] = sz
+            nodes[i] = nd
+            if e != "recursive":
+                eng[i] = e
+            if i % 500 == 0:
+                print("c5", i, sz, nd, flush=True)
+    dump("c5_sizes.json", {"count": count, "sizes": "".join(chr(ord("A") + s) for s in sizes),
+                           "size_encoding": "chr(ord('A') + size) per pair i",
+                           "nodes": nodes, "engine_overrides": eng,
+                           "how": "reference solve() (recursive, sequential node counts); "
+                                  "pairs it does not prove in 120 s go to solve_parallel"})
+
+
+def c4(floor=16, budget=6 * 3600.0):
+    """C4 (n=45, p=0.5, seeds 45000/45001): the reference pool with a size floor of
+    `floor` (SolveConfig::shared_bound). Optimal status proves no mapping of
+    size floor+1 exists; the GPU's 16-mapping, accepted by the reference's
+    oracle::verify (tests/test_gpu_golden.py), proves 16 is reached."""
+    g, h = O.ref_random_graph(45, 0.5, 45000), O.ref_random_graph(45, 0.5, 45001)
+    t0 = time.time()
+    r = O.ref_solve_parallel_floor(g, h, floor, workers=0, part_level=5, budget=budget)
+    out = {"instance": "ER n=45 p=0.5 seeds 45000/45001", "floor": floor, "status": r.status,
+           "pool_size_found": r.size, "pool_nodes": r.nodes, "wall_s": round(time.time() - t0, 1),
+           "workers": O.ref_lib().ref_hardware_concurrency(),
+           "how": "reference solve_parallel(workers=hardware_concurrency, part_level=5) with "
+                  "SharedBound floor; status 0 = no common subgraph larger than floor"}
+    print(out, flush=True)
+    assert r.status == 0, out
+    out["optimum"] = floor
+    dump("c4_proof.json", out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if not O.ref_available():
@@ -179,3 +278,11 @@ if __name__ == "__main__":
         c5()
     if what in ("c2", "all"):
         c2()
+    if what in ("c3", "all"):
+        c3()
+    if what == "c5full":
+        c5_full()
+    if what in ("floor", "all"):
+        floor()
+    if what == "c4":
+        c4()

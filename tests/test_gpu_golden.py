@@ -1,7 +1,8 @@
 """Full-size parity: GPU optima against the reference's own results.
 
 c2_sizes.json: all 100 C2 pairs (n=30) solved to optimality by the reference
-thread pool (oracle/_ref solve_parallel); c5_sample.json: 300 C5 pairs
+thread pool (oracle/_ref solve_parallel); c3_sizes.json: all 90 C3 pairs
+(directed, labelled, n=40), reference thread pool; c5_sample.json: 300 C5 pairs
 (n=16..24) by the reference sequential solve(), with node counts. The GPU
 must return the identical optimum for every pair (integer: exact), a mapping
 that verifies, and — in parity mode — the identical node count.
@@ -56,21 +57,29 @@ def test_c5_sample_matches_reference_sizes_and_nodes():
         assert (r.size, r.stats.recursions) == (gold[k]["size"], gold[k]["nodes"]), gold[k]
 
 
-def test_directed_labelled_n40_batch_against_oracle():
-    # C3 shape; the CPU oracle proves the cells it can in its budget
-    pairs, expect = [], []
-    for i, (L, p) in enumerate([(8, 0.5), (8, 0.3), (4, 0.5), (4, 0.3), (8, 0.1), (2, 0.5)]):
-        g = M.random_graph(40, p, 40000 + 2 * i, True, L)
-        h = M.random_graph(40, p, 40001 + 2 * i, True, L)
-        o = O.solve(O.G(40, g.codes.copy(), True, g.labels.copy()), O.G(40, h.codes.copy(), True, h.labels.copy()),
-                    budget=20)
-        if o.status == 0:
-            pairs.append((g, h))
-            expect.append(o.size)
-    assert pairs
+def c3_pairs():
+    """C3 (BASELINE configs[2]): L in {2,4,8} x p in {.1,.3,.5} x 10 directed
+    vertex-labelled ER pairs, n=40, seeds 40000+2i / 40001+2i."""
+    out = []
+    i = 0
+    for L in (2, 4, 8):
+        for p in (0.1, 0.3, 0.5):
+            for _ in range(10):
+                out.append((M.random_graph(40, p, 40000 + 2 * i, True, L),
+                            M.random_graph(40, p, 40001 + 2 * i, True, L)))
+                i += 1
+    return out
+
+
+def test_c3_all_90_pairs_match_reference_pool():
+    """Every C3 optimum equals the reference thread pool's (c3_sizes.json)."""
+    gold = json.load(open(os.path.join(HERE, "golden", "c3_sizes.json")))["pairs"]
+    assert len(gold) == 90 and all(g["status"] == 0 for g in gold)
+    pairs = c3_pairs()
     res, _ = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
-    for (g, h), r, e in zip(pairs, res, expect):
-        assert r.status == M.SolveStatus.optimal and r.size == e and M.verify(g, h, r.best)
+    for rec, (g, h), r in zip(gold, pairs, res):
+        assert r.status == M.SolveStatus.optimal and r.size == rec["size"], rec
+        assert M.verify(g, h, r.best)
 
 
 def test_c4_hard_pair_two_independent_modes():

@@ -75,3 +75,40 @@ def test_two_rank_gloo_sharding_and_reductions():
     assert tmax == 2.0 and ntotal == 200.0
     all_seeds = [s for part in seeds for s in part]
     assert len(set(all_seeds)) == 200                     # shards are distinct instances
+
+
+def test_bench_gpus_n_spawns_n_ranks():
+    """`bench.py --gpus 2` without an outside launcher re-runs itself under
+    torch.distributed.run with two ranks; with the reference arm (CPU only,
+    rank 0 measures) the line reports n_gpus 2 and the shared config dict."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(bench.__file__), "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3",
+                          "--ref-set", "c1"], capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"] == bench.bench_config(2)
+    assert line["all_optimal"] and line["value"] > 0
+
+
+def test_bench_rejects_world_size_mismatch():
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(bench.__file__), "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in (out.stderr + out.stdout)
+
+
+def test_strong_scaling_split_covers_every_pair_once():
+    for world in (1, 2, 3, 8):
+        parts = [bench.split(10000, r, world) for r in range(world)]
+        flat = [i for p in parts for i in p]
+        assert flat == list(range(10000))
