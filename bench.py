@@ -384,13 +384,19 @@ def side_configs(M, args, rank, world, ndev, device, barrier, max_over_ranks, su
                          "golden_ok": (r.size == opt) if opt is not None else None,
                          "golden": "c4_proof.json (reference pool: no 17 with floor 16; GPU 16-mapping "
                                    "accepted by the reference verify)" if proof else None}
-            members = ["gpu", "gpu+order=degree", "restarts:1", "gpu+order=components",
-                       "restarts:2", "gpu+order=block", "restarts:3", "restarts:4"][:max(world, 2)]
+            # one member per GPU (two on one GPU): orderings race in one launch
+            # spread over their GPUs; restarts / dead-end members are engines
+            # of their own; sizes are shared between all (share_incumbent)
+            members = ["gpu", "gpu+order=degree", "restarts:1", "jump:plus1+deadend=rel:4",
+                       "gpu+order=components", "restarts:2", "gpu+order=block", "restarts:3"][:max(world, 2)]
             t0 = time.perf_counter()
-            pr = M.run_portfolio(g, h, members, M.SolveConfig(device=device, devices=devs, budget_seconds=300))
+            pr = M.run_portfolio(g, h, members, M.SolveConfig(device=device, devices=devs),
+                                 M.PortfolioConfig(budget_seconds=300, share_incumbent=True))
             wall = time.perf_counter() - t0
             out["C4_portfolio"] = {"members": members, "n_gpus": world, "status": pr.status.name,
                                    "winner": pr.winner, "size": pr.size,
+                                   "engines": [{"spec": e.spec_name, "outcome": e.outcome, "size": e.size,
+                                                "wall_s": round(e.wall_seconds, 4)} for e in pr.engines],
                                    "time_to_optimum_s": pr.stats.kernel_seconds, "wall_s": wall,
                                    "nodes": pr.stats.recursions,
                                    "golden_ok": (pr.size == opt) if opt is not None else None}

@@ -13,6 +13,8 @@
  *                              (many pairs in one persistent launch)
  *   mcsg_solve_goal_directed   mcs::solve_goal_directed                   solve.hpp:132
  *   mcsg_bound_jump            mcs::bound_jump_search                     heuristics.hpp:69
+ *   mcsg_probe_parallel        bound_jump_search's bracket, probed in parallel (many targets
+ *                              per round, over GPUs)                      heuristics.cpp:114-185
  *   mcsg_portfolio             mcs::run_portfolio (race semantics)        portfolio.hpp:100
  *   mcsg_verify                mcs::oracle::verify                        oracle.hpp:16
  *   mcsg_random_graph          mcs::random_graph                          graph.hpp:99
@@ -114,6 +116,10 @@ typedef struct mcsg_options {
      * (atomic max) to the size of every mapping the search stores. floor_size
      * is the same floor fixed at call start. */
     volatile int32_t* shared_bound;
+    /* > 1: use 1/warp_share of the resident warps, so that several engines
+     * (one host thread each) can run concurrently on one GPU — concurrent
+     * calls on one device take separate device contexts. 0/1 = every warp. */
+    int32_t warp_share;
 } mcsg_options;
 
 #define MCSG_JUMP_PLUS_ONE 1
@@ -172,6 +178,17 @@ int32_t mcsg_solve_goal_directed(const mcsg_graph* g, const mcsg_graph* h,
 int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best,
                         int32_t doubling, const mcsg_options* opt, mcsg_result* out,
                         mcsg_stats* stats);
+/* Parallel binary search over goal probes (bound_jump_search's bracket,
+ * heuristics.cpp:114-185, probed `width` targets at a time): each round
+ * probes up to width (<= 32; 0 = max(8, devices)) targets of the open bracket
+ * (lower, upper] concurrently — dealt over opt->n_devices GPUs (one GPU when
+ * 0) as independent groups of one launch per device. A reached target implies
+ * every lower target, an exhausted one every higher target, across devices
+ * over NVLink P2P, so each probe stops once its answer is implied. Starts from
+ * current_best (a size known reachable); result.probes = targets probed.
+ * Throughput mode only. */
+int32_t mcsg_probe_parallel(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best, int32_t width,
+                            const mcsg_options* opt, mcsg_result* out, mcsg_stats* stats);
 /* Races `count` member strategies of ONE pair in one launch with a shared
  * incumbent size; first member to prove wins (portfolio.cpp:249-292).
  * orders[i] in MCSG_ORDER_*; seeds[i] != 0 gives member i a seeded search

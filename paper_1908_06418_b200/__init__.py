@@ -35,6 +35,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -98,7 +99,8 @@ class _Options(C.Structure):
                 ("seed", C.c_uint64), ("cancel", C.POINTER(C.c_int32)),
                 ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32),
                 ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32),
-                ("restart_multiplier", C.c_double), ("shared_bound", C.POINTER(C.c_int32))]
+                ("restart_multiplier", C.c_double), ("shared_bound", C.POINTER(C.c_int32)),
+                ("warp_share", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -138,6 +140,7 @@ def lib():
         L.mcsg_solve_goal_directed.argtypes = [G, G, O, R, S]
         L.mcsg_bound_jump.argtypes = [G, G, C.c_int32, C.c_int32, O, R, S]
         L.mcsg_portfolio.argtypes = [G, G, C.c_int32, P(C.c_int32), P(C.c_uint64), O, R, P(C.c_int32), S]
+        L.mcsg_probe_parallel.argtypes = [G, G, C.c_int32, C.c_int32, O, R, S]
         L.mcsg_verify.argtypes = [G, G, P(C.c_int32), C.c_int32]
         L.mcsg_random_graph.argtypes = [C.c_int32, C.c_double, C.c_uint64, C.c_uint32, C.c_int32,
                                         P(C.c_uint8), P(C.c_int32)]
@@ -410,6 +413,7 @@ class SolveConfig:
     deadend: tuple | None = None       # ("abs", n) | ("rel", mult): DeadEndPolicy
     deadend_jump: "JumpMode | None" = None  # jump that resumes after a suspect verdict
     restart_multiplier: float = 0.0    # RestartConfig::multiplier (throughput mode); 0 = no restarts
+    warp_share: int = 0                # > 1: use 1/warp_share of the GPU (concurrent engines on one GPU)
 
 
 @dataclass
@@ -506,6 +510,7 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
         if cfg.deadend_jump is not None:
             o.deadend_jump = 2 if cfg.deadend_jump == JumpMode.doubling else 1
     o.restart_multiplier = float(cfg.restart_multiplier)
+    o.warp_share = int(cfg.warp_share)
     for k, v in over.items():
         setattr(o, k, v)
     return o
@@ -722,30 +727,207 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
     return solve(g, h, dataclasses.replace(cfg, mode=MODE_PARITY))
 
 
+def probe_parallel(g: Graph, h: Graph, current_best: int = 0, width: int = 0,
+                   config: SolveConfig | None = None) -> SolveResult:
+    """Parallel binary search over goal probes (bound_jump_search's bracket,
+    heuristics.cpp:114-185, `width` targets per round, over config.devices):
+    a reached target implies every lower one, an exhausted one every higher
+    one, across GPUs over NVLink P2P. Throughput mode."""
+    import dataclasses
+    cfg = dataclasses.replace(config or SolveConfig(), mode=MODE_THROUGHPUT)
+    r, st = _Result(), _Stats()
+    _check(lib().mcsg_probe_parallel(C.byref(g._c()), C.byref(h._c()), int(current_best), int(width),
+                                     C.byref(_options(cfg)), C.byref(r), C.byref(st)))
+    return _result(r, st)
+
+
+@dataclass
+class PortfolioConfig:
+    """PortfolioConfig (portfolio.hpp:78-84)."""
+    mode: str = "race_all"              # "race_all" | "staged"
+    budget_seconds: float = 1e9
+    stage1_budget_seconds: float = 5.0
+    grace_seconds: float = 1.0          # cancellation acknowledgment watchdog
+    share_incumbent: bool = False       # monotone size broadcasts between engines (SharedBound)
+
+
+@dataclass
+class EngineReport:
+    """EngineReport (portfolio.hpp:68-75)."""
+    spec_name: str = ""
+    outcome: str = "finished"           # finished | cancelled | error | timeout
+    size: int = 0
+    wall_seconds: float = 0.0
+    cancel_ack_seconds: float = -1.0
+    error: str = ""
+
+
 @dataclass
 class PortfolioResult:
+    """PortfolioResult (portfolio.hpp:86-98)."""
     status: SolveStatus = SolveStatus.optimal
     winner: str = ""
     size: int = 0
     mapping: list = field(default_factory=list)
     wall_seconds: float = 0.0
     stats: SearchStats = field(default_factory=SearchStats)
+    engines: list = field(default_factory=list)   # EngineReport per member run
+    grace_violations: int = 0
+    overhead_seconds: float = 0.0
 
 
-def run_portfolio(g: Graph, h: Graph, specs, config: SolveConfig | None = None) -> PortfolioResult:
-    """run_portfolio (portfolio.cpp:310-365), race semantics on one GPU: every
-    member is an ordering of the same pair searched concurrently by the same
-    persistent kernel with a shared incumbent size; the first member to prove
-    optimality wins (portfolio.cpp:271-279)."""
-    specs = [parse_engine_spec(s) if isinstance(s, str) else s for s in specs]
-    if not specs:
-        raise GraphError("portfolio needs at least one engine spec")
+def _is_searcher(s: EngineSpec) -> bool:
+    """Plain searches (any ordering) race inside ONE GPU launch with a shared
+    incumbent size; every other member is an engine of its own."""
+    return (s.base in ("recursive", "iterative", "parallel", "gpu") and not s.goal_directed
+            and s.jump is None and s.deadend is None and s.restart_seed is None)
+
+
+def _race_group(g: Graph, h: Graph, specs, config: SolveConfig):
+    """The searchers of a portfolio in one launch (mcsg_portfolio): members are
+    orderings of the pair sharing the incumbent size; the first to prove wins."""
     orders = (C.c_int32 * len(specs))(*[int(s.order) for s in specs])
-    seeds = (C.c_uint64 * len(specs))(*[int(s.restart_seed or 0) for s in specs])
+    seeds = (C.c_uint64 * len(specs))(*[0 for _ in specs])
     r, st = _Result(), _Stats()
     win = C.c_int32(-1)
     _check(lib().mcsg_portfolio(C.byref(g._c()), C.byref(h._c()), len(specs), orders, seeds,
                                 C.byref(_options(config)), C.byref(r), C.byref(win), C.byref(st)))
     res = _result(r, st)
-    return PortfolioResult(res.status, specs[win.value].name() if win.value >= 0 else "", res.size,
-                           res.best, st.wall_s, res.stats)
+    return res, (specs[win.value].name() if win.value >= 0 else "")
+
+
+def _race(g, h, specs, cfg: SolveConfig, budget: float, bound, grace: float):
+    """race() (portfolio.cpp:249-292) over GPU engines: one host thread per
+    unit — the plain searchers together as one launch, every goal / jump /
+    dead-end / restarts member as its own engine (run_engine, GPU probes and
+    searches). Units are dealt over the configured devices; units sharing a
+    GPU split its warps (warp_share) and run concurrently. The first unit to
+    finish optimal wins and the others are cancelled (their cancel flag is
+    polled by the running kernels)."""
+    import dataclasses
+    import threading
+    searchers = [s for s in specs if _is_searcher(s)]
+    units = ([("group", searchers)] if searchers else []) + [("engine", s) for s in specs if not _is_searcher(s)]
+    devices = list(cfg.devices) if cfg.devices else [cfg.device]
+    # device placement: with a GPU per unit to spare, the searchers' launch
+    # spreads over every GPU the engines leave (P2P incumbent, first to prove
+    # stops all); otherwise units are dealt round-robin and share GPUs
+    n_eng = len(units) - (1 if searchers else 0)
+    if searchers and len(devices) >= len(units):
+        place = [devices[:len(devices) - n_eng]] + [[d] for d in devices[len(devices) - n_eng:]]
+    else:
+        place = [[devices[i % len(devices)]] for i in range(len(units))]
+    per_dev = {}
+    for pl in place:
+        for d in pl:
+            per_dev[d] = per_dev.get(d, 0) + 1
+    cancel = C.c_int32(0)
+    out = [None] * len(units)
+
+    def run(i):
+        kind, what = units[i]
+        dev = place[i][0]
+        ucfg = dataclasses.replace(cfg, device=dev, devices=tuple(place[i]) if len(place[i]) > 1 else (),
+                                   cancel=cancel, warp_share=per_dev[dev],
+                                   shared_bound=bound if bound is not None else cfg.shared_bound)
+        t0 = time.perf_counter()
+        try:
+            if kind == "group":
+                res, name = _race_group(g, h, what, dataclasses.replace(
+                    ucfg, budget_seconds=budget, mode=MODE_THROUGHPUT))
+            else:
+                b = min(what.budget_seconds, budget) if what.budget_seconds >= 0 else budget
+                res, name = run_engine(g, h, what, dataclasses.replace(ucfg, budget_seconds=b)), what.name()
+            out[i] = (res, name or (what.name() if kind == "engine" else ",".join(s.name() for s in what)),
+                      None, time.perf_counter())
+        except GraphError as e:
+            out[i] = (None, what.name() if kind == "engine" else "group", str(e), time.perf_counter())
+
+    t_start = time.perf_counter()
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(units))]
+    for t in threads:
+        t.start()
+    reports, seen = [], [False] * len(units)
+    winner = None
+    t_cancel = None
+    best = None
+    while not all(seen):
+        for i, t in enumerate(threads):
+            if seen[i] or t.is_alive():
+                continue
+            seen[i] = True
+            res, name, err, t_end = out[i]
+            rep = EngineReport(spec_name=name or (units[i][1].name() if units[i][0] == "engine" else ""),
+                               wall_seconds=t_end - t_start)
+            if err is not None:
+                rep.outcome, rep.error = "error", err
+            else:
+                rep.size = res.size
+                rep.outcome = {SolveStatus.optimal: "finished", SolveStatus.timeout: "timeout",
+                               SolveStatus.cancelled: "cancelled"}[res.status]
+                if res.status == SolveStatus.optimal and winner is None:
+                    winner = (name, res, rep.wall_seconds)
+                    cancel.value = 1
+                    t_cancel = time.perf_counter()
+                if best is None or res.size > best.size:
+                    best = res
+            if t_cancel is not None and (winner is None or winner[0] != rep.spec_name):
+                rep.cancel_ack_seconds = max(0.0, t_end - t_cancel)
+            reports.append(rep)
+        if not all(seen):
+            time.sleep(0.001)
+    grace_violations = sum(1 for r in reports if r.cancel_ack_seconds > grace)
+    return winner, best, reports, grace_violations
+
+
+def run_portfolio(g: Graph, h: Graph, specs, config: SolveConfig | None = None,
+                  portfolio: PortfolioConfig | None = None) -> PortfolioResult:
+    """run_portfolio (portfolio.cpp:310-365) on GPU engines. Every member
+    runs with its own semantics — plain searches race in one launch with a
+    shared incumbent size; goal-directed, bound-jump, dead-end and restarts
+    members run as their own GPU engines next to them — and the first member
+    to finish optimal wins (portfolio.cpp:271-279). Staged mode runs the
+    stage-1 members under stage1_budget_seconds, then stage 2 (everything
+    again when nothing is staged) with the rest of the budget, carrying the
+    best incumbent over. share_incumbent broadcasts sizes between the units
+    (SharedBound, solve.hpp:68-81)."""
+    specs = [parse_engine_spec(s) if isinstance(s, str) else s for s in specs]
+    if not specs:
+        raise GraphError("portfolio needs at least one engine spec")
+    for s in specs:
+        if s.base not in ("recursive",) and (s.goal_directed or s.jump is not None or s.restart_seed is not None):
+            raise GraphError("goal/jump/restart variants run on the recursive engine only")
+    cfg = config or SolveConfig()
+    pc = portfolio or PortfolioConfig(budget_seconds=cfg.budget_seconds)
+    t0 = time.perf_counter()
+    bound = SharedBound(0) if pc.share_incumbent else None
+    remaining = lambda: pc.budget_seconds - (time.perf_counter() - t0)  # noqa: E731
+    if pc.mode == "staged":
+        stage1 = [s for s in specs if s.stage <= 1]
+        stage2 = [s for s in specs if s.stage > 1]
+        winner, best, reports, gv = None, None, [], 0
+        if stage1 and pc.stage1_budget_seconds > 0:
+            winner, best, reports, gv = _race(g, h, stage1, cfg, min(pc.stage1_budget_seconds, pc.budget_seconds),
+                                              bound, pc.grace_seconds)
+        if winner is None:
+            w2, b2, r2, gv2 = _race(g, h, stage2 or stage1, cfg, max(0.0, remaining()), bound, pc.grace_seconds)
+            winner, reports, gv = w2, reports + r2, gv + gv2
+            if best is None or (b2 is not None and b2.size > best.size):
+                best = b2
+    elif pc.mode == "race_all":
+        winner, best, reports, gv = _race(g, h, specs, cfg, pc.budget_seconds, bound, pc.grace_seconds)
+    else:
+        raise GraphError(f"unknown portfolio mode '{pc.mode}'")
+    wall = time.perf_counter() - t0
+    res = PortfolioResult(engines=reports, grace_violations=gv, wall_seconds=wall)
+    if winner is not None:
+        name, r, w_wall = winner
+        res.status, res.winner, res.size, res.mapping, res.stats = SolveStatus.optimal, name, r.size, r.best, r.stats
+        res.overhead_seconds = wall - w_wall
+    else:
+        if all(r.outcome == "error" for r in reports):
+            raise GraphError("portfolio: every engine failed")
+        res.status = SolveStatus.timeout
+        if best is not None:
+            res.size, res.mapping, res.stats = best.size, best.best, best.stats
+    return res

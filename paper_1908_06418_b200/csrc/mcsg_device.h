@@ -179,6 +179,7 @@ struct Ctl {
 };
 
 constexpr int kMaxPeers = 16;
+constexpr int kMaxLadder = 32;  // probe targets of one parallel binary-search round
 
 struct KernelParams {
     const InstanceDesc* inst;   // n <= 64 kernels
@@ -230,6 +231,16 @@ struct KernelParams {
     // costs more than it saves); 0 = off
     int32_t compact;
     int32_t compact_hbm;  // the compact stack may sit in the HBM spill area (2: always, a test knob)
+    // Probe ladder (parallel binary search over goal probes):
+    // every group of the launch is a probe of the same pair with its own goal,
+    // and the ladder spans every device of the round. Entry k (ascending goal)
+    // is ladder_grp[k], local or a peer's GroupState over NVLink P2P. A probe
+    // that reaches its goal marks every entry with a goal <= its own reached
+    // (and done); a probe that exhausts its tree without reaching marks every
+    // entry with a goal >= its own done (failed). ladder_n = 0: no ladder.
+    int32_t ladder_n;
+    int32_t ladder_goal[kMaxLadder];
+    GroupState* ladder_grp[kMaxLadder];
 };
 
 }  // namespace mcsg

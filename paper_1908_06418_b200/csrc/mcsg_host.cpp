@@ -52,6 +52,7 @@ void ck(cudaError_t e, const char* what) {
 constexpr uint32_t kRingCap = 16384;                      // power of two
 constexpr uint32_t kWideRingCap = 4096;                   // wide slots are 17 KB
 constexpr int kSpillClasses = kMaxDepth * kMaxN;          // 64-bit kernel: worst-case stack, no overflow possible
+constexpr int kMaxSlots = 4;                              // contexts per device for concurrent host threads
 
 // Bitset width of the kernel flavour that fits n vertices.
 int bits_for(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
@@ -304,6 +305,8 @@ struct LaunchExtras {
     bool relabeled = false;          // jobs already in the kernel's vertex order
     int seed_best = 0;               // host incumbent of instance 0 (frontier expansion)
     std::vector<uint8_t> seed_v, seed_u;
+    std::vector<int> ladder_goal;            // probe ladder of the round (ascending goals)
+    std::vector<GroupState*> ladder_grp;     // its groups: local or peer GroupState
 };
 
 // A launch in flight on one context (ctx.mu held by the caller until finish()).
@@ -359,6 +362,7 @@ void plan(Context& ctx, const std::vector<Job>& jobs, const mcsg_options& o, InF
     if (blocks <= 0) throw Error("requested shared-memory class stack does not fit");
     int ctas = blocks * ctx.sms;
     if (o.max_warps > 0) ctas = std::min(ctas, (o.max_warps + kWarpsPerCta - 1) / kWarpsPerCta);
+    if (o.warp_share > 1) ctas = std::max(1, ctas / o.warp_share);  // concurrent engines on one GPU
     if (parity) ctas = std::min(ctas, (int(jobs.size()) + kWarpsPerCta - 1) / kWarpsPerCta);
     f->ctas = std::max(ctas, 1);
     f->warps = f->ctas * kWarpsPerCta;
@@ -481,6 +485,12 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     if (p.n_peers > kMaxPeers) throw Error("too many peer devices");
     for (int q = 0; q < p.n_peers; ++q) p.peer_grp[q] = ex.peers[q];
     p.peer_done_on_complete = ex.peer_done_on_complete ? 1 : 0;
+    if (ex.ladder_goal.size() > size_t(kMaxLadder)) throw Error("too many probe targets in one round");
+    p.ladder_n = int(ex.ladder_goal.size());
+    for (int k = 0; k < p.ladder_n; ++k) {
+        p.ladder_goal[k] = ex.ladder_goal[k];
+        p.ladder_grp[k] = ex.ladder_grp[k];
+    }
     p.cancel = o.cancel ? ctx.d_cancel : nullptr;
     p.ext_floor = o.shared_bound ? ctx.d_xfloor : nullptr;
     p.ext_best = o.shared_bound ? ctx.d_xbest : nullptr;
@@ -609,9 +619,23 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
         out.groups.resize(n_groups);
         return out;
     }
-    Context& ctx = context(o.device);
-    std::lock_guard<std::mutex> lock(ctx.mu);
-    InFlight f = start(ctx, jobs, n_groups, o, LaunchExtras{});
+    // Calls from several host threads on one device (portfolio members racing
+    // as separate engines) each take a free context slot — own stream, ring
+    // and state — so their launches run concurrently (each sized by
+    // warp_share); a thread only waits when every slot is busy.
+    int dev = o.device;
+    if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
+    Context* ctx = nullptr;
+    for (int slot = 0; slot < kMaxSlots && !ctx; ++slot) {
+        Context& c = context(dev, slot);
+        if (c.mu.try_lock()) ctx = &c;
+    }
+    if (!ctx) {
+        ctx = &context(dev, 0);
+        ctx->mu.lock();
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu, std::adopt_lock);
+    InFlight f = start(*ctx, jobs, n_groups, o, LaunchExtras{});
     return finish(f);
 }
 
@@ -626,11 +650,19 @@ struct DevicePlan {
     std::vector<TaskSlot> seeded;
     std::vector<WideSlot> wseeded;
     bool roots = true;
+    int n_groups = 1;
+};
+
+// Probe ladder of a parallel binary-search round: entry k (ascending goal)
+// is group `group[k]` of plan `plan[k]`.
+struct Ladder {
+    std::vector<int> plan, group, goal;
 };
 
 std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_options& o,
                                     bool peer_done_on_complete, int seed_best,
-                                    const std::vector<uint8_t>& seed_v, const std::vector<uint8_t>& seed_u) {
+                                    const std::vector<uint8_t>& seed_v, const std::vector<uint8_t>& seed_u,
+                                    const Ladder* ladder = nullptr) {
     const int D = int(plans.size());
     std::vector<Context*> ctxs(D);
     std::map<int, int> used;
@@ -660,7 +692,7 @@ std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_o
         oo.mode = MCSG_MODE_THROUGHPUT;
         plan(*ctxs[i], plans[i].jobs, oo, &shape);
         ck(cudaSetDevice(ctxs[i]->device), "cudaSetDevice");
-        ctxs[i]->reserve(plans[i].jobs.size(), 1, shape.spill_bytes);
+        ctxs[i]->reserve(plans[i].jobs.size(), size_t(plans[i].n_groups), shape.spill_bytes);
     }
     std::vector<InFlight> fl(D);
     for (int i = 0; i < D; ++i) {
@@ -670,15 +702,22 @@ std::vector<LaunchOut> launch_multi(std::vector<DevicePlan>& plans, const mcsg_o
         ex.roots = plans[i].roots;
         ex.relabeled = true;
         ex.peer_done_on_complete = peer_done_on_complete;
-        for (int j = 0; j < D; ++j)
-            if (j != i) ex.peers.push_back(ctxs[j]->d_grp);
+        if (ladder) {  // probes of different goals share no incumbent: only the ladder
+            for (size_t k = 0; k < ladder->goal.size(); ++k) {
+                ex.ladder_goal.push_back(ladder->goal[k]);
+                ex.ladder_grp.push_back(ctxs[ladder->plan[k]]->d_grp + ladder->group[k]);
+            }
+        } else {
+            for (int j = 0; j < D; ++j)
+                if (j != i) ex.peers.push_back(ctxs[j]->d_grp);
+        }
         ex.seed_best = seed_best;
         ex.seed_v = seed_v;
         ex.seed_u = seed_u;
         mcsg_options oo = o;
         oo.mode = MCSG_MODE_THROUGHPUT;
         oo.device = ctxs[i]->device;
-        fl[i] = start(*ctxs[i], plans[i].jobs, 1, oo, ex);
+        fl[i] = start(*ctxs[i], plans[i].jobs, plans[i].n_groups, oo, ex);
     }
     std::vector<LaunchOut> out(D);
     for (int i = 0; i < D; ++i) out[i] = finish(fl[i]);
@@ -1250,6 +1289,157 @@ int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t curren
         if (stats) {
             stats->probes = probes;
             stats->wall_s = secs_since(t0);
+        }
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Parallel binary search over goal probes (the GPU form of
+// bound_jump_search's bracket, heuristics.cpp:114-185): every round probes up
+// to `width` targets of the open bracket (lower, upper] at once, dealt over
+// the devices, each target a group of its device's launch. Inside a round a
+// reached target marks every lower one reached and an exhausted one marks
+// every higher one failed, across devices over NVLink P2P (probe ladder), so
+// each probe stops as soon as its answer is implied.
+int32_t mcsg_probe_parallel(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best, int32_t width,
+                            const mcsg_options* opt, mcsg_result* out, mcsg_stats* stats) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        mcsg_options o = defaults(opt);
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        if (o.budget_s <= 0) {
+            timed_out(out);
+            return MCSG_TIMEOUT;
+        }
+        if (o.mode == MCSG_MODE_PARITY) throw Error("probe ladders run in throughput mode");
+        if (o.n_devices > 16) throw Error("at most 16 devices");
+        std::vector<int> devs;
+        if (o.n_devices > 0)
+            for (int i = 0; i < o.n_devices; ++i) devs.push_back(o.devices[i]);
+        else
+            devs.push_back(o.device);
+        if (width <= 0) width = std::max<int>(8, int(devs.size()));
+        width = std::min(width, kMaxLadder);
+        Job base = make_job(G, H, o.order);
+        relabel_for_throughput(base, o.seed);
+        long long lower = std::max(0, current_best), upper = std::min(G.n, H.n);
+        if (lower > upper) throw Error("current best exceeds the smaller graph");
+        const bool unlimited = o.budget_s >= 1e8;
+        JobResult wit;
+        int status = MCSG_OPTIMAL;
+        uint64_t probes = 0, nodes = 0;
+        LaunchOut agg;
+        bool first = true;
+        double ktot = 0;
+        // one round over the given ascending targets; false when stopped
+        auto round = [&](const std::vector<int>& targets) -> bool {
+            const int K = int(targets.size());
+            const int D = std::min<int>(int(devs.size()), K);
+            std::vector<DevicePlan> plans(D);
+            Ladder lad;
+            for (int d = 0; d < D; ++d) {
+                plans[d].device = devs[d] < 0 ? 0 : devs[d];
+                plans[d].n_groups = 0;
+            }
+            if (devs[0] < 0) ck(cudaGetDevice(&plans[0].device), "cudaGetDevice");
+            for (int k = 0; k < K; ++k) {
+                DevicePlan& pl = plans[k % D];
+                Job j = base;
+                j.goal = targets[k];
+                j.group = pl.n_groups;
+                lad.plan.push_back(k % D);
+                lad.group.push_back(pl.n_groups);
+                lad.goal.push_back(targets[k]);
+                pl.jobs.push_back(std::move(j));
+                pl.n_groups += 1;
+            }
+            mcsg_options oo = o;
+            oo.goal = 0;
+            oo.deadend_abs = 0;
+            oo.deadend_rel = 0;
+            oo.deadend_jump = 0;
+            oo.restart_multiplier = 0;
+            if (!unlimited) {
+                oo.budget_s = o.budget_s - secs_since(t0);
+                if (oo.budget_s <= 0) {
+                    status = MCSG_TIMEOUT;
+                    return false;
+                }
+            }
+            std::vector<LaunchOut> outs = launch_multi(plans, oo, false, 0, {}, {}, &lad);
+            probes += uint64_t(K);
+            long long lo2 = lower, up2 = upper;
+            bool stopped = false;
+            for (int k = 0; k < K; ++k) {
+                const JobResult& r = outs[lad.plan[k]].jobs[lad.group[k]];
+                const GroupResult& gr = outs[lad.plan[k]].groups[lad.group[k]];
+                nodes += r.nodes;
+                if (r.size > wit.size) wit = r;
+                if (gr.reached) lo2 = std::max<long long>(lo2, targets[k]);
+                else if (r.status == MCSG_OPTIMAL && gr.done) up2 = std::min<long long>(up2, targets[k] - 1);
+                else if (r.status != MCSG_OPTIMAL) {
+                    stopped = true;
+                    status = r.status;
+                }
+            }
+            for (LaunchOut& lo : outs) {
+                if (first) {
+                    agg = lo;
+                    first = false;
+                } else {
+                    agg.counters.nodes += lo.counters.nodes;
+                    agg.counters.donations += lo.counters.donations;
+                    agg.counters.tasks += lo.counters.tasks;
+                    agg.counters.busy_cycles += lo.counters.busy_cycles;
+                    agg.counters.idle_cycles += lo.counters.idle_cycles;
+                    agg.launches += lo.launches;
+                    agg.h2d_bytes += lo.h2d_bytes;
+                    agg.d2h_bytes += lo.d2h_bytes;
+                }
+            }
+            double kmax = 0;
+            for (LaunchOut& lo : outs) kmax = std::max(kmax, lo.kernel_s);
+            ktot += kmax;  // rounds run one after another; devices of a round concurrently
+            if (stopped) return false;
+            lo2 = std::max<long long>(lo2, wit.size);  // a stored mapping proves its size
+            if (lo2 < lower || up2 > upper || lo2 > up2) throw Error("bound jump bracket violated");
+            lower = lo2;
+            upper = up2;
+            return true;
+        };
+        bool ok = true;
+        // Targets of a round: the first half just above the bracket's floor
+        // (the incumbent is usually close to the optimum: plus_one's jumps, in
+        // parallel), the rest spaced geometrically up to its ceiling (doubling's
+        // reach: high goals fail fast, so they cost little).
+        while (ok && lower < upper) {
+            const long long span = upper - lower;
+            const int K = int(std::min<long long>(width, span));
+            const int hcons = (K + 1) / 2, geo = K - hcons;
+            std::vector<int> targets;
+            for (int k = 1; k <= hcons; ++k) targets.push_back(int(lower + k));
+            for (int i = 1; i <= geo; ++i) {
+                const long long rest = span - hcons;
+                const long long num = rest * ((1ll << i) - 1), den = (1ll << geo) - 1;
+                const int t = int(lower + hcons + (num + den - 1) / den);
+                if (t > targets.back()) targets.push_back(t);
+            }
+            ok = round(targets);
+        }
+        if (ok && wit.size < lower && lower > 0) round({int(lower)});  // a witness for a supplied size
+        JobResult r = wit;  // (finish() already mapped it back to original ids)
+        r.status = status;
+        r.nodes = nodes;
+        write_result(G, H, r, out);
+        out->probes = int32_t(probes);
+        if (stats && !first) {
+            agg.kernel_s = ktot;
+            fill_stats(stats, agg, secs_since(t0), probes);
+            stats->nodes = nodes;
         }
         return out->status;
     } catch (const std::exception& e) {

@@ -192,6 +192,9 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 __device__ __forceinline__ int ld_volatile(const int32_t* p) {
     return *reinterpret_cast<const volatile int32_t*>(p);
 }
+__device__ __forceinline__ int ld_volatile_i(const int32_t* p) {
+    return *reinterpret_cast<const volatile int32_t*>(p);
+}
 __device__ __forceinline__ unsigned ld_volatile_u(const uint32_t* p) {
     return *reinterpret_cast<const volatile uint32_t*>(p);
 }
