@@ -120,6 +120,15 @@ typedef struct mcsg_options {
      * (one host thread each) can run concurrently on one GPU — concurrent
      * calls on one device take separate device contexts. 0/1 = every warp. */
     int32_t warp_share;
+    /* DeadEndPolicy::Kind (heuristics.hpp:30-38): 0 = from the fields above
+     * (deadend_abs > 0 absolute, deadend_rel > 0 relative), 1 absolute
+     * (deadend_abs may then be 0: every node is suspect), 2 relative. Parity
+     * mode runs the reference's monitor per node (note_recursion /
+     * deadend_check before the node's offer, search_core.hpp:133-141): with a
+     * jump it stops at the reference's node, without one it counts suspect
+     * nodes (result.deadend_suspects). Throughput mode checks at polls and
+     * only stops when a jump follows. */
+    int32_t deadend_kind;
 } mcsg_options;
 
 #define MCSG_JUMP_PLUS_ONE 1
@@ -161,6 +170,7 @@ typedef struct mcsg_result {
     double solve_s;          /* device time from launch to this instance's proof */
     int32_t flags;           /* MCSG_RESULT_SUSPECT: stopped by the dead-end policy */
     int32_t probes;          /* goal / jump probes run for this result */
+    uint64_t deadend_suspects; /* SearchStats::deadend_suspects (parity mode: suspect nodes) */
 } mcsg_result;
 
 #define MCSG_RESULT_SUSPECT 1

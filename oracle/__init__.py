@@ -59,7 +59,7 @@ class _RefResult(C.Structure):
                 ("recursions", C.c_uint64), ("probes", C.c_uint64), ("restarts", C.c_uint64),
                 ("visited_ranges", C.c_uint64), ("tasks_published", C.c_uint64),
                 ("double_executions", C.c_uint64), ("wall_seconds", C.c_double),
-                ("error", C.c_char * 256)]
+                ("error", C.c_char * 256), ("deadend_suspects", C.c_uint64)]
 
 
 @dataclass
@@ -281,7 +281,8 @@ def _ref_res(r: _RefResult) -> Result:
     pairs = [(r.pairs[2 * i], r.pairs[2 * i + 1]) for i in range(r.size)]
     return Result(r.status, r.size, pairs, r.recursions, r.probes, r.wall_seconds,
                   dict(restarts=r.restarts, visited_ranges=r.visited_ranges,
-                       tasks_published=r.tasks_published, double_executions=r.double_executions))
+                       tasks_published=r.tasks_published, double_executions=r.double_executions,
+                       deadend_suspects=r.deadend_suspects))
 
 
 def ref_run_engine(g: G, h: G, spec="recursive", budget=1e9, disable_pruning=False) -> Result:

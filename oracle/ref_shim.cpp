@@ -52,6 +52,7 @@ struct ref_result {
     uint64_t double_executions;
     double wall_seconds;
     char error[256];
+    uint64_t deadend_suspects;
 };
 }
 
@@ -92,6 +93,7 @@ void fill(const mcs::SolveResult& r, ref_result* out) {
     out->double_executions = r.stats.iteration_double_executions;
     out->wall_seconds = r.stats.wall_seconds;
     out->error[0] = 0;
+    out->deadend_suspects = r.stats.deadend_suspects;
 }
 
 void fail(ref_result* out, const char* what) {

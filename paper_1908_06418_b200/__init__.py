@@ -100,7 +100,7 @@ class _Options(C.Structure):
                 ("n_devices", C.c_int32), ("devices", C.c_int32 * 16), ("frontier", C.c_int32),
                 ("deadend_abs", C.c_uint64), ("deadend_rel", C.c_double), ("deadend_jump", C.c_int32),
                 ("restart_multiplier", C.c_double), ("shared_bound", C.POINTER(C.c_int32)),
-                ("warp_share", C.c_int32)]
+                ("warp_share", C.c_int32), ("deadend_kind", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -118,7 +118,7 @@ class _Stats(C.Structure):
 class _Result(C.Structure):
     _fields_ = [("status", C.c_int32), ("size", C.c_int32), ("pairs", C.c_int32 * (2 * MAX_N)),
                 ("nodes", C.c_uint64), ("solve_s", C.c_double), ("flags", C.c_int32),
-                ("probes", C.c_int32)]
+                ("probes", C.c_int32), ("deadend_suspects", C.c_uint64)]
 
 
 _lib = None
@@ -503,8 +503,10 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
         kind, val = cfg.deadend
         if kind == "abs":
             o.deadend_abs = int(val)
+            o.deadend_kind = 1
         elif kind == "rel":
             o.deadend_rel = float(val)
+            o.deadend_kind = 2
         else:
             raise GraphError(f"unknown deadend policy '{kind}'")
         if cfg.deadend_jump is not None:
@@ -519,7 +521,7 @@ def _options(cfg: SolveConfig | None, **over) -> _Options:
 def _result(r: _Result, st: _Stats | None = None, seed: int = 0) -> SolveResult:
     pairs = [(int(r.pairs[2 * i]), int(r.pairs[2 * i + 1])) for i in range(r.size)]
     s = SearchStats(recursions=int(r.nodes), solve_seconds=r.solve_s, seed=seed, probes=int(r.probes),
-                    deadend_suspects=int(r.flags & 1))
+                    deadend_suspects=int(r.deadend_suspects))
     if st is not None:
         s.wall_seconds = st.wall_s
         s.kernel_seconds = st.kernel_s
@@ -717,11 +719,14 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
         return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, seed=spec.restart_seed,
                                                restart_multiplier=2.0))
     if spec.deadend is not None:
-        # forecast-then-mitigate (portfolio.cpp:136-155): a monitored all-warp
-        # solve; with a jump configured, a suspect verdict hands the incumbent
-        # to the bound jump (without one the monitor never stops the search)
-        return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, deadend=spec.deadend,
-                                               deadend_jump=spec.jump))
+        # forecast-then-mitigate (portfolio.cpp:136-155): a monitored solve;
+        # with a jump configured, a suspect verdict hands the incumbent to the
+        # bound jump (without one the monitor never stops the search). An
+        # explicit parity-mode config runs the reference's per-node monitor
+        # (its recursions, probes and suspects); otherwise the all-warp engine
+        # monitors at its polls.
+        mode = MODE_PARITY if cfg.mode == MODE_PARITY else MODE_THROUGHPUT
+        return solve(g, h, dataclasses.replace(cfg, mode=mode, deadend=spec.deadend, deadend_jump=spec.jump))
     if spec.jump is not None:
         return bound_jump_search(g, h, 0, spec.jump, cfg)
     return solve(g, h, dataclasses.replace(cfg, mode=MODE_PARITY))

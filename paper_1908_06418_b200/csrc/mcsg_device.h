@@ -46,17 +46,20 @@ struct InstanceDesc {
     uint16_t vkey[kMaxN];   // (255 - deg) << 6 | id: min == select_vertex (label_classes.cpp:69-78)
 };
 
-// Per-instance mutable state (results).
-struct InstanceState {
+// Per-instance mutable state (results). 16-byte aligned: polls prefetch its
+// first 16 bytes with cp.async (which faults on a misaligned source).
+struct alignas(16) InstanceState {
     uint32_t map_size;      // size of the mapping stored in map_v/map_u
     int32_t lock;           // spin lock guarding map_* on improvement
     int32_t open_tasks;     // tasks of this instance not yet finished
     int32_t workers;        // warps currently running a task of this instance (fairness)
     unsigned long long nodes;
     unsigned long long t_done_ns;  // %globaltimer when the last task finished
+    unsigned long long suspects;   // parity mode: nodes the dead-end monitor found suspect
     uint8_t map_v[kMaxWideN + 1];
     uint8_t map_u[kMaxWideN + 1];
 };
+static_assert(sizeof(InstanceState) % 16 == 0, "InstanceState rows must stay 16-byte aligned");
 
 // Wide instance description (n <= 255): same header fields as InstanceDesc,
 // rows of kWideWords words (the 128-vertex kernel reads the first two).
@@ -216,8 +219,10 @@ struct KernelParams {
     // dead-end policy (DeadEndPolicy, heuristics.hpp:30-38; deadend_check,
     // heuristics.cpp:103-112): suspect when nodes since the last improvement
     // reach deadend_abs, or deadend_rel * max(1, nodes at the improvement)
-    unsigned long long deadend_abs;  // 0 = off
-    double deadend_rel;              // 0 = off
+    int32_t deadend_kind;            // 0 off, 1 absolute, 2 relative
+    int32_t deadend_stop;            // 1: a suspect node stops the search (a jump follows)
+    unsigned long long deadend_abs;  // absolute threshold
+    double deadend_rel;              // relative multiplier
     // Restarts (RestartConfig::multiplier, heuristics.hpp:90-102): a restart
     // is due when the group's nodes since its last improvement reach
     // restart_mult x max(1, nodes at that improvement); every warp of the

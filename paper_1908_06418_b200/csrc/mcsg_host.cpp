@@ -208,6 +208,7 @@ struct JobResult {
     double solve_s = 0;
     bool completed = false;
     bool suspect = false;  // the dead-end policy stopped it
+    uint64_t suspects = 0;  // parity mode: suspect nodes (deadend_suspects)
 };
 
 struct GroupResult {
@@ -289,6 +290,12 @@ void bump_shared(volatile int32_t* sb, int32_t size) {
     int32_t cur = __atomic_load_n(sb, __ATOMIC_ACQUIRE);
     while (size > cur && !__atomic_compare_exchange_n(sb, &cur, size, true, __ATOMIC_RELEASE, __ATOMIC_ACQUIRE)) {
     }
+}
+
+// Effective DeadEndPolicy kind of the options (0 = no policy).
+int deadend_kind(const mcsg_options& o) {
+    if (o.deadend_kind == 1 || o.deadend_kind == 2) return o.deadend_kind;
+    return o.deadend_abs ? 1 : o.deadend_rel > 0 ? 2 : 0;
 }
 
 double secs_since(std::chrono::steady_clock::time_point t0) {
@@ -506,7 +513,12 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     }
     p.counters = ctx.d_cnt;
     if (!parity) p.restart_mult = o.restart_multiplier;
-    if (!parity && o.deadend_jump != 0) {  // the monitor only stops when a jump follows
+    // Dead-end monitor: per node in parity mode (stop when a jump follows,
+    // else count suspect nodes); at polls in throughput mode, and only when a
+    // jump follows (it then stops the launch).
+    if (const int dk = deadend_kind(o); dk && (parity || o.deadend_jump != 0)) {
+        p.deadend_kind = dk;
+        p.deadend_stop = o.deadend_jump != 0 ? 1 : 0;
         p.deadend_abs = o.deadend_abs;
         p.deadend_rel = o.deadend_rel;
     }
@@ -588,6 +600,7 @@ LaunchOut finish(InFlight& f) {
         const Job& j = (*f.jobs)[i];
         r.completed = s.open_tasks == 0;
         r.nodes = s.nodes;
+        r.suspects = s.suspects;
         r.size = int(s.map_size);
         r.solve_s = s.t_done_ns > out.counters.t_start_ns ? (s.t_done_ns - out.counters.t_start_ns) * 1e-9 : 0.0;
         const bool group_done = out.groups[j.group].done;
@@ -888,6 +901,7 @@ void write_result(const HostGraph& g, const HostGraph& h, const JobResult& r, mc
     out->nodes = r.nodes;
     out->solve_s = r.solve_s;
     out->flags = r.suspect ? MCSG_RESULT_SUSPECT : 0;
+    out->deadend_suspects = r.suspects ? r.suspects : (r.suspect ? 1 : 0);
     if (r.size > 0 && verify(g, h, r.pairs.data(), r.size) != 1)
         throw Error("internal error: kernel returned an invalid mapping");
     for (int k = 0; k < 2 * r.size; ++k) out->pairs[k] = r.pairs[k];
@@ -1029,7 +1043,7 @@ static int32_t solve_plain(const mcsg_graph* g, const mcsg_graph* h, const mcsg_
 int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
                    mcsg_result* out, mcsg_stats* stats) {
     const mcsg_options o = defaults(opt);
-    if (o.deadend_jump != 0 && (o.deadend_abs || o.deadend_rel > 0)) {
+    if (o.deadend_jump != 0 && deadend_kind(o)) {
         // forecast-then-mitigate (portfolio.cpp:136-155): monitored solve; on a
         // suspect verdict the bound jump resumes from the incumbent size
         const auto t0 = std::chrono::steady_clock::now();
@@ -1052,6 +1066,7 @@ int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options*
         }
         out->nodes += first.nodes;
         out->flags = MCSG_RESULT_SUSPECT;
+        out->deadend_suspects = first.deadend_suspects;
         if (stats) {
             stats->nodes += st2.nodes;
             stats->probes = st2.probes;
@@ -1100,6 +1115,7 @@ int32_t mcsg_portfolio(const mcsg_graph* g, const mcsg_graph* h, int32_t count,
         lo_opt.deadend_abs = 0;
         lo_opt.deadend_rel = 0;
         lo_opt.deadend_jump = 0;
+        lo_opt.deadend_kind = 0;
         std::vector<JobResult> members(count);
         bool done = false;
         int w = -1;
@@ -1362,6 +1378,7 @@ int32_t mcsg_probe_parallel(const mcsg_graph* g, const mcsg_graph* h, int32_t cu
             oo.deadend_abs = 0;
             oo.deadend_rel = 0;
             oo.deadend_jump = 0;
+            oo.deadend_kind = 0;
             oo.restart_multiplier = 0;
             if (!unlimited) {
                 oo.budget_s = o.budget_s - secs_since(t0);

@@ -183,6 +183,25 @@ def floor():
     dump("floor.json", {"cases": out})
 
 
+def deadend():
+    """Dead-end handling (DeadEndMonitor / deadend_check, heuristics.cpp:103-112;
+    forecast-then-jump, portfolio.cpp:136-155): monitored solves with and
+    without a jump, absolute and relative policies. recursions, probes and
+    deadend_suspects are deterministic (sequential engines)."""
+    out = []
+    specs = ["recursive+deadend=abs:50", "recursive+deadend=rel:1.5", "jump:plus1+deadend=abs:200",
+             "jump:double+deadend=abs:1000", "jump:plus1+deadend=rel:2", "jump:double+deadend=rel:0.5",
+             "jump:plus1+deadend=abs:0", "recursive+deadend=abs:0"]
+    for n, d, s in random_pairs(16, 8, 22, 6060):
+        g, h = O.ref_random_graph(n, d, s), O.ref_random_graph(n, d, s + 1)
+        for spec in specs:
+            r = O.ref_run_engine(g, h, spec)
+            out.append({"n": n, "d": d, "seed": s, "spec": spec, "status": r.status, "size": r.size,
+                        "nodes": r.nodes, "probes": r.probes, "suspects": r.extra["deadend_suspects"],
+                        "pairs": [list(p) for p in r.pairs]})
+    dump("deadend.json", {"cases": out})
+
+
 def c3_pairs():
     """C3 (BASELINE configs[2]): directed vertex-labelled ER n=40,
     L in {2,4,8} x p in {.1,.3,.5} x 10 pairs, seeds 40000+2i / 40001+2i."""
@@ -284,5 +303,7 @@ if __name__ == "__main__":
         c5_full()
     if what in ("floor", "all"):
         floor()
+    if what in ("deadend", "all"):
+        deadend()
     if what == "c4":
         c4()

@@ -71,6 +71,25 @@ def c3_pairs():
     return out
 
 
+def test_c5_all_10000_pairs_match_reference():
+    """Every C5 optimum (10,000 ER pairs, n=16..24) equals the reference's
+    (c5_sizes.json: sequential solve(), the pool for the rare long pair), in
+    one all-warp launch."""
+    gold = json.load(open(os.path.join(HERE, "golden", "c5_sizes.json")))
+    sizes = gold["sizes"]
+    assert gold["count"] == 10000 and len(sizes) == 10000
+    pairs = []
+    for i in range(10000):
+        n = 16 + (i // 3) % 9
+        p = (0.1, 0.3, 0.5)[i % 3]
+        pairs.append((M.random_graph(n, p, 50000 + 2 * i), M.random_graph(n, p, 50001 + 2 * i)))
+    res, st = M.solve_batch(pairs, M.SolveConfig(mode=M.MODE_THROUGHPUT))
+    bad = [i for i, r in enumerate(res) if r.status != M.SolveStatus.optimal or r.size != ord(sizes[i]) - ord("A")]
+    assert not bad, bad[:10]
+    for i in range(0, 10000, 97):
+        assert M.verify(*pairs[i], res[i].best)
+
+
 def test_c3_all_90_pairs_match_reference_pool():
     """Every C3 optimum equals the reference thread pool's (c3_sizes.json)."""
     gold = json.load(open(os.path.join(HERE, "golden", "c3_sizes.json")))["pairs"]
