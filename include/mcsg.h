@@ -15,6 +15,9 @@
  *   mcsg_bound_jump            mcs::bound_jump_search                     heuristics.hpp:69
  *   mcsg_probe_parallel        bound_jump_search's bracket, probed in parallel (many targets
  *                              per round, over GPUs)                      heuristics.cpp:114-185
+ *   mcsg_solve_with_restarts   mcs::solve_with_restarts                   heuristics.hpp:107
+ *                              (parity mode: the reference's RestartDriver exactly — seeded
+ *                               segment draws, recursions, restarts, visited ranges)
  *   mcsg_portfolio             mcs::run_portfolio (race semantics)        portfolio.hpp:100
  *   mcsg_verify                mcs::oracle::verify                        oracle.hpp:16
  *   mcsg_random_graph          mcs::random_graph                          graph.hpp:99
@@ -43,7 +46,7 @@
 extern "C" {
 #endif
 
-#define MCSG_ABI_VERSION 4
+#define MCSG_ABI_VERSION 5
 
 /* status codes (mirror mcs_main.cpp:22-24 exit codes; SolveStatus solve.hpp:23) */
 #define MCSG_OPTIMAL 0
@@ -160,6 +163,7 @@ typedef struct mcsg_stats {
     double idle_s;           /* idle_cycles / the device's SM clock (SearchStats::idle_seconds) */
     double busy_s;           /* busy_cycles / the device's SM clock */
     uint64_t peer_pushes;    /* incumbent improvements pushed to peer GPUs over NVLink P2P */
+    uint64_t visited_ranges; /* SearchStats::visited_ranges (mcsg_solve_with_restarts) */
 } mcsg_stats;
 
 typedef struct mcsg_result {
@@ -199,6 +203,22 @@ int32_t mcsg_bound_jump(const mcsg_graph* g, const mcsg_graph* h, int32_t curren
  * Throughput mode only. */
 int32_t mcsg_probe_parallel(const mcsg_graph* g, const mcsg_graph* h, int32_t current_best, int32_t width,
                             const mcsg_options* opt, mcsg_result* out, mcsg_stats* stats);
+/* mcs::solve_with_restarts (heuristics.hpp:107, restarts.cpp:195-246).
+ * opt->restart_multiplier is RestartConfig::multiplier (<= 0: no restarts) and
+ * opt->seed RestartConfig::seed. MCSG_MODE_PARITY reproduces the reference's
+ * RestartDriver exactly: the segment pool is drawn with the reference's seeded
+ * mt19937_64, each segment runs on the GPU with the per-node restart check,
+ * and result/stats carry the reference's recursions, restarts and
+ * visited_ranges; ranges_out (may be NULL; ranges_cap int32 words) receives
+ * the VisitedRanges runs in insertion order, each run as [len(lo), lo...,
+ * len(hi), hi...] — a PositionKey is the iteration taken at each depth
+ * (heuristics.hpp:77), INT32_MAX for successor({}) — and *ranges_len the words
+ * needed. MCSG_MODE_THROUGHPUT runs the work-sharing engine's restart epochs
+ * (every warp freezes its open path into the ring); visited_ranges = 1 for a
+ * completed search. */
+int32_t mcsg_solve_with_restarts(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                                 mcsg_result* out, mcsg_stats* stats, int32_t* ranges_out, int64_t ranges_cap,
+                                 int64_t* ranges_len);
 /* Races `count` member strategies of ONE pair in one launch with a shared
  * incumbent size; first member to prove wins (portfolio.cpp:249-292).
  * orders[i] in MCSG_ORDER_*; seeds[i] != 0 gives member i a seeded search

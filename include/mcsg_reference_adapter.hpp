@@ -169,6 +169,53 @@ inline SolveResult bound_jump_search(const Graph& g, const Graph& h, int current
     return to_result(r, st);
 }
 
+// mcs::solve_with_restarts (heuristics.hpp:107). MCSG_MODE_PARITY (the
+// default here) is the reference's RestartDriver exactly: the same seeded
+// segment draws, recursions, restarts and visited ranges; with
+// config.ranges_out the VisitedRanges runs are filled in the reference's order.
+inline SolveResult solve_with_restarts(const Graph& g, const Graph& h, const RestartConfig& config,
+                                       int mode = MCSG_MODE_PARITY) {
+    if (config.visitor) throw GraphError("mcs::gpu: NodeVisitor hooks are not supported on the GPU engine");
+    GraphBuffer gb(g), hb(h);
+    SolveConfig base;
+    base.budget_seconds = config.budget_seconds;
+    base.order = config.order;
+    base.disable_pruning = config.disable_pruning;
+    base.shared_bound = config.shared_bound;
+    mcsg_options o = to_options(base, mode);
+    o.seed = config.seed;
+    o.restart_multiplier = config.multiplier;
+    CancelBridge bridge(config.cancel, o, config.shared_bound);
+    mcsg_result r{};
+    mcsg_stats st{};
+    std::vector<int32_t> words(config.ranges_out ? size_t(1) << 16 : 0);
+    int64_t need = 0;
+    check(mcsg_solve_with_restarts(&gb.view, &hb.view, &o, &r, &st, words.data(), int64_t(words.size()), &need));
+    if (config.ranges_out && need > int64_t(words.size())) {  // deterministic: again with room
+        words.resize(size_t(need));
+        check(mcsg_solve_with_restarts(&gb.view, &hb.view, &o, &r, &st, words.data(), need, &need));
+    }
+    SolveResult out = to_result(r, st);
+    out.stats.recursions = st.nodes;
+    out.stats.restarts = st.restarts;
+    out.stats.visited_ranges = st.visited_ranges;
+    out.stats.seed = config.seed;
+    if (config.ranges_out) {
+        auto key = [&](size_t& i) {
+            PositionKey k;
+            const int32_t len = words[i++];
+            for (int32_t d = 0; d < len; ++d) k.emplace_back(d, words[i++]);
+            return k;
+        };
+        for (size_t i = 0; i < size_t(need);) {
+            PositionKey lo = key(i);
+            PositionKey hi = key(i);
+            config.ranges_out->add(std::move(lo), std::move(hi));
+        }
+    }
+    return out;
+}
+
 // oracle::verify (oracle.hpp:16) through the library's host verifier.
 inline bool verify(const Graph& g, const Graph& h, const Mapping& m) {
     GraphBuffer gb(g), hb(h);

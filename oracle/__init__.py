@@ -118,6 +118,9 @@ def orc_lib():
         lib.orc_bound_jump.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_int, C.c_int,
                                        P(_OrcOptions), P(_OrcResult)]
         lib.orc_verify.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32), C.c_int]
+        lib.orc_solve_with_restarts.argtypes = [P(_OrcGraph), P(_OrcGraph), P(_OrcOptions), C.c_uint64,
+                                                C.c_double, P(_OrcResult), P(C.c_uint64), P(C.c_int32),
+                                                C.c_int64, P(C.c_int64)]
         lib.orc_bruteforce.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32)]
         _orc = lib
     return _orc
@@ -147,6 +150,9 @@ def ref_lib():
         lib.ref_solve_parallel_floor.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_int, C.c_int,
                                                  C.c_double, C.c_int, P(_RefResult)]
         lib.ref_verify.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32), C.c_int]
+        lib.ref_solve_with_restarts.argtypes = [P(_OrcGraph), P(_OrcGraph), C.c_uint64, C.c_double, C.c_int,
+                                                C.c_int, C.c_double, P(_RefResult), P(C.c_int32), C.c_int64,
+                                                P(C.c_int64)]
         lib.ref_bruteforce.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32)]
         lib.ref_ordering.argtypes = [P(_OrcGraph), C.c_int, P(C.c_int32)]
         lib.ref_refine_chain.argtypes = [P(_OrcGraph), P(_OrcGraph), P(C.c_int32), C.c_int,
@@ -232,6 +238,69 @@ def bound_jump(g: G, h: G, current_best=0, doubling=False, budget=1e9, order=0) 
                                 C.byref(_opts(budget, order=order)), C.byref(r)) != 0:
         raise ValueError("oracle: invalid graph pair")
     return _res(r)
+
+
+def decode_ranges(words):
+    """[len(lo), lo..., len(hi), hi...] runs -> [(lo, hi)] PositionKeys as
+    lists of (depth, iteration) pairs (heuristics.hpp:77)."""
+    keys, i = [], 0
+    while i < len(words):
+        k = int(words[i])
+        keys.append([(d, int(words[i + 1 + d])) for d in range(k)])
+        i += 1 + k
+    return [(keys[j], keys[j + 1]) for j in range(0, len(keys), 2)]
+
+
+def _words(call):
+    """Runs call(buf, cap, len_ptr) with a growing buffer; returns the words."""
+    cap = 1 << 16
+    while True:
+        buf = (C.c_int32 * cap)()
+        need = C.c_int64(0)
+        call(buf, cap, C.byref(need))
+        if need.value <= cap:
+            return list(buf[:need.value])
+        cap = need.value
+
+
+def solve_with_restarts(g: G, h: G, seed=1, multiplier=2.0, prune=True, order=0, budget=1e9, floor_size=0):
+    """solve_with_restarts restated (restarts.cpp:195-246): Result with
+    extra restarts / visited_ranges / ranges."""
+    gs, hs = g.c_struct(), h.c_struct()
+    out = {}
+
+    def call(buf, cap, need):
+        r = _OrcResult()
+        rs = C.c_uint64(0)
+        if orc_lib().orc_solve_with_restarts(C.byref(gs), C.byref(hs), C.byref(_opts(budget, 0, prune, order,
+                                                                                      floor_size)),
+                                             seed, multiplier, C.byref(r), C.byref(rs), buf, cap, need) != 0:
+            raise ValueError("oracle: invalid graph pair")
+        out["r"], out["restarts"] = r, rs.value
+
+    words = _words(call)
+    r = out["r"]
+    res = Result(r.status, r.size, [(r.pairs[2 * i], r.pairs[2 * i + 1]) for i in range(r.size)], r.nodes, 0,
+                 r.wall_s)
+    res.extra = dict(restarts=out["restarts"], visited_ranges=int(r.probes), ranges=decode_ranges(words))
+    return res
+
+
+def ref_solve_with_restarts(g: G, h: G, seed=1, multiplier=2.0, prune=True, order=0, budget=1e9) -> Result:
+    """The unmodified reference's solve_with_restarts (with the VisitedRanges sink)."""
+    gs, hs = g.c_struct(), h.c_struct()
+    out = {}
+
+    def call(buf, cap, need):
+        r = _RefResult()
+        ref_lib().ref_solve_with_restarts(C.byref(gs), C.byref(hs), seed, multiplier, int(not prune), order,
+                                          budget, C.byref(r), buf, cap, need)
+        out["r"] = r
+
+    words = _words(call)
+    res = _ref_res(out["r"])
+    res.extra["ranges"] = decode_ranges(words)
+    return res
 
 
 def ordering(g: G, strategy: int):

@@ -824,3 +824,389 @@ int orc_bruteforce(const orc_graph* g, const orc_graph* h, int32_t* pairs_out) {
         if (bf_subsets(g, h, chosen, 0, 0, k, pairs_out)) return k;
     return 0;
 }
+
+/* --------------------------------------------------------- restarts -- */
+/* std::mt19937_64 (the segment draw of solve_with_restarts, restarts.cpp:213). */
+typedef struct {
+    uint64_t s[312];
+    int i;
+} mt64;
+
+static void mt64_seed(mt64* m, uint64_t seed) {
+    m->s[0] = seed;
+    for (int k = 1; k < 312; ++k)
+        m->s[k] = 6364136223846793005ull * (m->s[k - 1] ^ (m->s[k - 1] >> 62)) + (uint64_t)k;
+    m->i = 312;
+}
+
+static uint64_t mt64_next(mt64* m) {
+    if (m->i >= 312) {
+        for (int k = 0; k < 312; ++k) {
+            uint64_t y = (m->s[k] & 0xFFFFFFFF80000000ull) | (m->s[(k + 1) % 312] & 0x7FFFFFFFull);
+            uint64_t x = m->s[(k + 156) % 312] ^ (y >> 1);
+            if (y & 1u) x ^= 0xB5026F5AA96619E9ull;
+            m->s[k] = x;
+        }
+        m->i = 0;
+    }
+    uint64_t y = m->s[m->i++];
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+
+/* PositionKey (heuristics.hpp:77) without the depth field (it equals the
+ * index): the iteration taken at each depth. */
+typedef struct {
+    int32_t* it;
+    int len;
+} pkey;
+
+static pkey key_dup(const int32_t* it, int len, int extra) {
+    pkey k;
+    k.it = malloc(sizeof(int32_t) * (size_t)(len + extra + 1));
+    if (len) memcpy(k.it, it, sizeof(int32_t) * (size_t)len);
+    k.len = len;
+    return k;
+}
+
+/* extend / successor, restarts.cpp:13-24 */
+static pkey key_extend(const int32_t* it, int len, int x) {
+    pkey k = key_dup(it, len, 1);
+    k.it[k.len++] = x;
+    return k;
+}
+
+static pkey key_successor(const int32_t* it, int len) {
+    if (len == 0) {
+        pkey k = key_dup(it, 0, 1);
+        k.it[k.len++] = 2147483647;
+        return k;
+    }
+    pkey k = key_dup(it, len, 0);
+    k.it[len - 1] += 1;
+    return k;
+}
+
+/* Segment (restarts.cpp:26-33): a frozen node's state plus the first
+ * iteration still to run. */
+typedef struct {
+    int* left;
+    int* right;
+    cls_t* dom;
+    int nd;
+    int32_t* map; /* (v,u) pairs */
+    int nmap;
+    pkey pos;
+    int from;
+} rseg;
+
+typedef struct {
+    const orc_graph* g;
+    const orc_graph* h;
+    int* deg;
+    int ng, nh;
+    int prune;
+    int64_t maxp, floor_size;
+    struct timespec deadline;
+    int unlimited;
+    const volatile int32_t* cancel;
+    double mult;
+    int best_n;
+    int32_t* best_pairs;
+    int cur_n;
+    int32_t* cur_pairs;
+    uint64_t nodes, restarts, at;
+    int rflag;
+    int reason; /* 0 none, 1 timeout, 2 cancelled, 4 max reached */
+    rseg* pool;
+    int npool, cappool;
+    pkey* rlo;
+    pkey* rhi;
+    int nranges, capranges;
+} rctx;
+
+static void r_add_range(rctx* c, pkey lo, pkey hi) {
+    if (c->nranges == c->capranges) {
+        c->capranges = c->capranges ? 2 * c->capranges : 64;
+        c->rlo = realloc(c->rlo, sizeof(pkey) * (size_t)c->capranges);
+        c->rhi = realloc(c->rhi, sizeof(pkey) * (size_t)c->capranges);
+    }
+    c->rlo[c->nranges] = lo;
+    c->rhi[c->nranges] = hi;
+    c->nranges++;
+}
+
+static void r_push(rctx* c, const int* left, const int* right, const cls_t* dom, int nd, const int32_t* pos,
+                   int npos, int from) {
+    if (c->npool == c->cappool) {
+        c->cappool = c->cappool ? 2 * c->cappool : 64;
+        c->pool = realloc(c->pool, sizeof(rseg) * (size_t)c->cappool);
+    }
+    rseg* s = &c->pool[c->npool++];
+    s->left = malloc(sizeof(int) * (size_t)(c->ng + 1));
+    s->right = malloc(sizeof(int) * (size_t)(c->nh + 1));
+    memcpy(s->left, left, sizeof(int) * (size_t)c->ng);
+    memcpy(s->right, right, sizeof(int) * (size_t)c->nh);
+    s->dom = malloc(sizeof(cls_t) * (size_t)(nd + 1));
+    memcpy(s->dom, dom, sizeof(cls_t) * (size_t)nd);
+    s->nd = nd;
+    s->map = malloc(sizeof(int32_t) * (size_t)(2 * c->cur_n + 1));
+    memcpy(s->map, c->cur_pairs, sizeof(int32_t) * (size_t)(2 * c->cur_n));
+    s->nmap = c->cur_n;
+    s->pos = key_dup(pos, npos, 0);
+    s->from = from;
+}
+
+static void r_poll(rctx* c) { /* RestartDriver::poll, restarts.cpp:61-66 */
+    if (c->cancel && *c->cancel)
+        c->reason = 2;
+    else if ((c->nodes & 0xffu) == 1 && !c->unlimited && now_past(&c->deadline))
+        c->reason = 1;
+}
+
+static int r_restart_due(const rctx* c) { /* restarts.cpp:68-72 */
+    uint64_t delta = c->nodes - c->at;
+    return (double)delta >= c->mult * (double)(c->at > 1 ? c->at : 1);
+}
+
+/* RestartDriver::node, restarts.cpp:80-190. `dom` is this node's own copy. */
+static void r_node(rctx* c, cls_t* dom, int nd, int* left, int* right, const int32_t* pos, int npos, int from,
+                   int is_root) {
+    if (c->reason) return;
+    ++c->nodes;
+    r_poll(c);
+    if (c->reason) return;
+    if (c->mult > 0 && !c->rflag && r_restart_due(c)) { /* :87-91 */
+        c->rflag = 1;
+        ++c->restarts;
+        c->at = c->nodes;
+    }
+    if (c->rflag) { /* :92-95 freeze this whole node */
+        r_push(c, left, right, dom, nd, pos, npos, from);
+        return;
+    }
+    if (c->cur_n > c->best_n) { /* :97 inc.offer */
+        c->best_n = c->cur_n;
+        memcpy(c->best_pairs, c->cur_pairs, sizeof(int32_t) * 2 * (size_t)c->cur_n);
+        c->at = c->nodes;
+    }
+    int64_t bound = bound_of(c->cur_n, dom, nd);
+    /* lo = from == 0 ? pos : extend(pos, from)   (:107) */
+    pkey lo = from == 0 ? key_dup(pos, npos, 0) : key_extend(pos, npos, from);
+    if (c->prune && c->cur_n >= c->maxp) { /* :108-111 */
+        c->reason = 4;
+        free(lo.it);
+        return;
+    }
+    int64_t inc = c->best_n > c->floor_size ? c->best_n : c->floor_size;
+    if (c->prune && bound <= inc) { /* :112-115 */
+        if (is_root)
+            r_add_range(c, lo, key_successor(pos, npos));
+        else
+            free(lo.it);
+        return;
+    }
+    int bi = select_class(dom, nd, left); /* :117-121 */
+    if (bi < 0) {
+        if (is_root)
+            r_add_range(c, lo, key_successor(pos, npos));
+        else
+            free(lo.it);
+        return;
+    }
+    cls_t* entry = NULL; /* :124-125 entry state, for freezing */
+    if (c->mult > 0) {
+        entry = malloc(sizeof(cls_t) * (size_t)(nd + 1));
+        memcpy(entry, dom, sizeof(cls_t) * (size_t)nd);
+    }
+    cls_t* bd = &dom[bi];
+    int v = select_vertex(bd, left, c->deg); /* :128-134 */
+    for (int j = 0; j < bd->ll; ++j)
+        if (left[bd->ls + j] == v) {
+            int t = left[bd->ls + bd->ll - 1];
+            left[bd->ls + bd->ll - 1] = v;
+            left[bd->ls + j] = t;
+            break;
+        }
+    bd->ll--;
+    const int total = bd->rl;
+    const int n_iters = total + 1;
+    bd->rl--;
+    int last_u = -1;
+    for (int skip = 0; skip < (from < total ? from : total); ++skip) { /* :140-147 */
+        int next = -1;
+        for (int j = 0; j < total; ++j) {
+            int cand = right[bd->rs + j];
+            if (cand > last_u && (next == -1 || cand < next)) next = cand;
+        }
+        last_u = next;
+    }
+    /* children get their own class copies; filter() partitions the windows */
+    ctx_t fc;
+    memset(&fc, 0, sizeof(fc));
+    fc.g = c->g;
+    fc.h = c->h;
+    fc.left = left;
+    fc.right = right;
+    orc_result dummy;
+    memset(&dummy, 0, sizeof(dummy));
+    fc.stats = &dummy;
+    cls_t* child = malloc(sizeof(cls_t) * (size_t)(4 * nd + 4));
+    for (int it = from; it < n_iters; ++it) { /* :149-187 */
+        if (it < total) {
+            int pj = -1;
+            for (int j = 0; j < total; ++j) {
+                int cand = right[bd->rs + j];
+                if (cand > last_u && (pj == -1 || cand < right[bd->rs + pj])) pj = j;
+            }
+            int u = right[bd->rs + pj];
+            last_u = u;
+            right[bd->rs + pj] = right[bd->rs + total - 1];
+            right[bd->rs + total - 1] = u;
+            int k = filter(&fc, dom, nd, v, u, child);
+            cls_t* cc = malloc(sizeof(cls_t) * (size_t)(k + 1));
+            memcpy(cc, child, sizeof(cls_t) * (size_t)k);
+            c->cur_pairs[2 * c->cur_n] = v;
+            c->cur_pairs[2 * c->cur_n + 1] = u;
+            c->cur_n++;
+            pkey ep = key_extend(pos, npos, it);
+            r_node(c, cc, k, left, right, ep.it, ep.len, 0, 0);
+            free(ep.it);
+            free(cc);
+            c->cur_n--;
+        } else { /* :165-175 v left unmatched */
+            bd->rl++;
+            cls_t* rest = malloc(sizeof(cls_t) * (size_t)(nd + 1));
+            memcpy(rest, dom, sizeof(cls_t) * (size_t)nd);
+            int nr = nd;
+            if (rest[bi].ll == 0) {
+                rest[bi] = rest[nr - 1];
+                nr--;
+            }
+            pkey ep = key_extend(pos, npos, it);
+            r_node(c, rest, nr, left, right, ep.it, ep.len, 0, 0);
+            free(ep.it);
+            free(rest);
+            bd->rl--;
+        }
+        if (c->rflag || c->reason) { /* :176-186 */
+            if (c->rflag) {
+                r_push(c, left, right, entry, nd, pos, npos, it + 1);
+                r_add_range(c, lo, key_extend(pos, npos, it));
+                lo.it = NULL;
+            }
+            bd->rl++;
+            free(lo.it);
+            free(entry);
+            free(child);
+            return;
+        }
+    }
+    bd->rl++;
+    free(entry);
+    free(child);
+    if (is_root)
+        r_add_range(c, lo, key_successor(pos, npos));
+    else
+        free(lo.it);
+}
+
+/* solve_with_restarts, restarts.cpp:195-246. */
+int orc_solve_with_restarts(const orc_graph* g, const orc_graph* h, const orc_options* o, uint64_t seed,
+                            double multiplier, orc_result* r, uint64_t* restarts, int32_t* ranges_out,
+                            int64_t ranges_cap, int64_t* ranges_len) {
+    memset(r, 0, sizeof(*r));
+    if (restarts) *restarts = 0;
+    if (ranges_len) *ranges_len = 0;
+    if (check_graphs(g, h)) {
+        r->status = -1;
+        return -1;
+    }
+    if (o->budget_s <= 0) {
+        r->status = 1;
+        return 0;
+    }
+    struct timespec t0;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    ordered_t ord;
+    order_begin(g, h, o->order, &ord);
+    rctx c;
+    memset(&c, 0, sizeof(c));
+    c.g = &ord.g2;
+    c.h = &ord.h2;
+    c.ng = ord.g2.n;
+    c.nh = ord.h2.n;
+    c.prune = o->prune;
+    c.maxp = c.ng < c.nh ? c.ng : c.nh;
+    c.floor_size = o->floor_size;
+    c.cancel = o->cancel;
+    c.mult = multiplier;
+    {
+        ctx_t dl;
+        set_deadline(&dl, o->budget_s);
+        c.deadline = dl.deadline;
+        c.unlimited = dl.unlimited;
+    }
+    c.deg = malloc(sizeof(int) * (size_t)(c.ng + 1));
+    for (int v = 0; v < c.ng; ++v) c.deg[v] = orc_degree(c.g, v);
+    c.best_pairs = r->pairs;
+    c.cur_pairs = malloc(sizeof(int32_t) * (size_t)(2 * (c.ng + c.nh) + 2));
+    /* the initial segment (restarts.cpp:214-216) */
+    {
+        ctx_t ic;
+        memset(&ic, 0, sizeof(ic));
+        ic.g = c.g;
+        ic.h = c.h;
+        int* left = malloc(sizeof(int) * (size_t)(c.ng + 1));
+        int* right = malloc(sizeof(int) * (size_t)(c.nh + 1));
+        ic.left = left;
+        ic.right = right;
+        cls_t* init = malloc(sizeof(cls_t) * (size_t)(c.ng + 1));
+        int nc = initial(&ic, init);
+        r_push(&c, left, right, init, nc, NULL, 0, 0);
+        free(left), free(right), free(init);
+    }
+    mt64 rng;
+    mt64_seed(&rng, seed);
+    while (c.npool > 0 && !c.reason) { /* :218-228 */
+        int idx = c.npool == 1 ? 0 : (int)(mt64_next(&rng) % (uint64_t)c.npool);
+        rseg s = c.pool[idx];
+        memmove(&c.pool[idx], &c.pool[idx + 1], sizeof(rseg) * (size_t)(c.npool - idx - 1));
+        c.npool--;
+        c.rflag = 0;
+        memcpy(c.cur_pairs, s.map, sizeof(int32_t) * 2 * (size_t)s.nmap);
+        c.cur_n = s.nmap;
+        r_node(&c, s.dom, s.nd, s.left, s.right, s.pos.it, s.pos.len, s.from, 1);
+        free(s.left), free(s.right), free(s.dom), free(s.map), free(s.pos.it);
+    }
+    for (int i = 0; i < c.npool; ++i)
+        free(c.pool[i].left), free(c.pool[i].right), free(c.pool[i].dom), free(c.pool[i].map),
+            free(c.pool[i].pos.it);
+    free(c.pool);
+    int64_t w = 0;
+    for (int i = 0; i < c.nranges; ++i)
+        for (int side = 0; side < 2; ++side) {
+            const pkey* k = side ? &c.rhi[i] : &c.rlo[i];
+            if (ranges_out && w < ranges_cap) ranges_out[w] = k->len;
+            ++w;
+            for (int d = 0; d < k->len; ++d) {
+                if (ranges_out && w < ranges_cap) ranges_out[w] = k->it[d];
+                ++w;
+            }
+        }
+    if (ranges_len) *ranges_len = w;
+    for (int i = 0; i < c.nranges; ++i) free(c.rlo[i].it), free(c.rhi[i].it);
+    free(c.rlo), free(c.rhi);
+    order_end(&ord, r->pairs, c.best_n);
+    r->size = c.best_n;
+    r->nodes = c.nodes;
+    r->status = c.reason == 1 ? 1 : c.reason == 2 ? 2 : 0;
+    r->probes = (uint64_t)c.nranges; /* (visited_ranges travels in probes) */
+    if (restarts) *restarts = c.restarts;
+    r->wall_s = elapsed(&t0);
+    free(c.deg), free(c.cur_pairs);
+    return 0;
+}

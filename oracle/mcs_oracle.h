@@ -66,6 +66,14 @@ int orc_solve_goal_directed(const orc_graph* g, const orc_graph* h, const orc_op
 /* mcs::bound_jump_search (proj/src/heuristics.cpp:114-185); doubling 0 = plus_one. */
 int orc_bound_jump(const orc_graph* g, const orc_graph* h, int current_best, int doubling,
                    const orc_options* o, orc_result* r);
+/* mcs::solve_with_restarts (proj/src/restarts.cpp:195-246): seeded segment
+ * draws (mt19937_64), restart rule, visited ranges. r->probes carries
+ * stats.visited_ranges; ranges_out (may be NULL) receives each run as
+ * [len(lo), lo..., len(hi), hi...] (iterations per depth), *ranges_len the
+ * words needed. */
+int orc_solve_with_restarts(const orc_graph* g, const orc_graph* h, const orc_options* o, uint64_t seed,
+                            double multiplier, orc_result* r, uint64_t* restarts, int32_t* ranges_out,
+                            int64_t ranges_cap, int64_t* ranges_len);
 /* mcs::oracle::verify (proj/src/oracle.cpp:8-24): 1 valid, 0 invalid, -1 out of range. */
 int orc_verify(const orc_graph* g, const orc_graph* h, const int32_t* pairs, int k);
 /* mcs::oracle::mcs_bruteforce (proj/src/oracle.cpp:76-86): size, or -1 above n=10. */

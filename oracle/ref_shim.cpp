@@ -9,6 +9,7 @@
 //   mcs::parse_engine_spec       proj/include/mcs/portfolio.hpp:34
 //   mcs::run_engine              proj/include/mcs/portfolio.hpp:37
 //   mcs::solve_parallel          proj/include/mcs/engine_parallel.hpp:16 (optionally with a SharedBound floor)
+//   mcs::solve_with_restarts     proj/include/mcs/heuristics.hpp:107 (with the VisitedRanges sink)
 //   mcs::oracle::verify          proj/include/mcs/oracle.hpp:16
 //   mcs::oracle::mcs_bruteforce  proj/include/mcs/oracle.hpp:26
 //   mcs::make_ordering           proj/include/mcs/heuristics.hpp:26
@@ -146,6 +147,45 @@ int ref_run_engine(const ref_graph* g, const ref_graph* h, const char* spec, dou
         cfg.disable_pruning = disable_pruning != 0;
         mcs::SolveResult r = mcs::run_engine(gg, hh, mcs::parse_engine_spec(spec), cfg);
         fill(r, out);
+        return 0;
+    } catch (const std::exception& e) {
+        fail(out, e.what());
+        return -1;
+    }
+}
+
+// mcs::solve_with_restarts (heuristics.hpp:107) with the VisitedRanges sink:
+// ranges_out receives each run as [len(lo), lo iterations..., len(hi), hi
+// iterations...] (a PositionKey's depth field equals its index, so only the
+// iterations travel); *ranges_len = the words needed.
+int ref_solve_with_restarts(const ref_graph* g, const ref_graph* h, uint64_t seed, double multiplier,
+                            int disable_pruning, int order, double budget, ref_result* out, int32_t* ranges_out,
+                            int64_t ranges_cap, int64_t* ranges_len) {
+    try {
+        mcs::Graph gg = to_graph(g), hh = to_graph(h);
+        mcs::RestartConfig rc;
+        rc.seed = seed;
+        rc.multiplier = multiplier;
+        rc.disable_pruning = disable_pruning != 0;
+        rc.order = static_cast<mcs::OrderingStrategy>(order);
+        rc.budget_seconds = budget;
+        mcs::VisitedRanges vr;
+        rc.ranges_out = &vr;
+        fill(mcs::solve_with_restarts(gg, hh, rc), out);
+        int64_t w = 0;
+        auto put = [&](int32_t x) {
+            if (ranges_out && w < ranges_cap) ranges_out[w] = x;
+            ++w;
+        };
+        for (const auto& run : vr.runs)
+            for (const mcs::PositionKey* k : {&run.first, &run.second}) {
+                put(int32_t(k->size()));
+                for (size_t d = 0; d < k->size(); ++d) {
+                    if ((*k)[d].first != int(d)) throw std::runtime_error("position key depth != index");
+                    put((*k)[d].second);
+                }
+            }
+        if (ranges_len) *ranges_len = w;
         return 0;
     } catch (const std::exception& e) {
         fail(out, e.what());

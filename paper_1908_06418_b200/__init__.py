@@ -50,7 +50,7 @@ __all__ = [
     "SolveConfig", "SearchStats", "SolveResult", "solve", "solve_parallel", "solve_batch",
     "solve_goal_directed", "bound_jump_search", "make_ordering", "EngineSpec", "parse_engine_spec",
     "run_engine", "PortfolioResult", "run_portfolio", "verify", "pack_graph", "lib", "device_count",
-    "MODE_THROUGHPUT", "MODE_PARITY",
+    "MODE_THROUGHPUT", "MODE_PARITY", "RestartConfig", "VisitedRanges", "solve_with_restarts",
 ]
 
 
@@ -112,7 +112,7 @@ class _Stats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64),
                 ("busy_cycles", C.c_uint64), ("idle_cycles", C.c_uint64),
                 ("restarts", C.c_uint64), ("frozen", C.c_uint64), ("idle_s", C.c_double),
-                ("busy_s", C.c_double), ("peer_pushes", C.c_uint64)]
+                ("busy_s", C.c_double), ("peer_pushes", C.c_uint64), ("visited_ranges", C.c_uint64)]
 
 
 class _Result(C.Structure):
@@ -141,6 +141,7 @@ def lib():
         L.mcsg_bound_jump.argtypes = [G, G, C.c_int32, C.c_int32, O, R, S]
         L.mcsg_portfolio.argtypes = [G, G, C.c_int32, P(C.c_int32), P(C.c_uint64), O, R, P(C.c_int32), S]
         L.mcsg_probe_parallel.argtypes = [G, G, C.c_int32, C.c_int32, O, R, S]
+        L.mcsg_solve_with_restarts.argtypes = [G, G, O, R, S, P(C.c_int32), C.c_int64, P(C.c_int64)]
         L.mcsg_verify.argtypes = [G, G, P(C.c_int32), C.c_int32]
         L.mcsg_random_graph.argtypes = [C.c_int32, C.c_double, C.c_uint64, C.c_uint32, C.c_int32,
                                         P(C.c_uint8), P(C.c_int32)]
@@ -607,6 +608,101 @@ def bound_jump_search(g: Graph, h: Graph, current_best: int, mode: JumpMode,
     return _result(r, st)
 
 
+# ---------------------------------------------------------------- restarts --
+_KEY_MAX = 2**31 - 1
+
+
+class VisitedRanges:
+    """VisitedRanges (heuristics.hpp:79-89, heuristics.cpp:187-210): half-open
+    lexicographic intervals of PositionKeys — a key is the list of
+    (depth, iteration) pairs along a node's path from the root."""
+
+    def __init__(self):
+        self.runs = []
+
+    def add(self, lo, hi):
+        self.runs.append((list(lo), list(hi)))
+
+    def normalize(self) -> bool:
+        """Sorts and merges touching runs; False if any two overlap."""
+        self.runs.sort()
+        disjoint = True
+        merged = []
+        for lo, hi in self.runs:
+            if merged and lo < merged[-1][1]:
+                disjoint = False
+            if merged and lo == merged[-1][1]:
+                merged[-1] = (merged[-1][0], hi)
+            else:
+                merged.append((lo, hi))
+        self.runs = merged
+        return disjoint
+
+    def covers(self, key) -> bool:
+        key = list(key)
+        return any(not (key < lo) and key < hi for lo, hi in self.runs)
+
+    def size(self) -> int:
+        return len(self.runs)
+
+
+@dataclass
+class RestartConfig:
+    """RestartConfig (heuristics.hpp:92-104) plus the GPU engine knobs.
+
+    mode MODE_PARITY (default) reproduces the reference's RestartDriver
+    exactly — seeded mt19937_64 segment draws, recursions, restarts, visited
+    ranges — one GPU warp per segment; MODE_THROUGHPUT runs the all-warp
+    engine's restart epochs (open paths frozen into the task ring)."""
+    seed: int = 1
+    multiplier: float = 2.0            # <= 0: restarts off
+    budget_seconds: float = 1e9
+    order: OrderingStrategy = OrderingStrategy.none
+    cancel: object = None
+    disable_pruning: bool = False
+    shared_bound: "int | SharedBound" = 0
+    ranges_out: "VisitedRanges | None" = None  # instrumentation sink
+    mode: int = MODE_PARITY
+    device: int = -1
+
+
+def solve_with_restarts(g: Graph, h: Graph, config: RestartConfig | None = None) -> SolveResult:
+    """mcs::solve_with_restarts (heuristics.hpp:107, restarts.cpp:195-246)."""
+    cfg = config or RestartConfig()
+    sc = SolveConfig(budget_seconds=cfg.budget_seconds, order=cfg.order, cancel=cfg.cancel,
+                     disable_pruning=cfg.disable_pruning, shared_bound=cfg.shared_bound, mode=cfg.mode,
+                     device=cfg.device, seed=cfg.seed, restart_multiplier=cfg.multiplier)
+    o = _options(sc)
+    want = cfg.ranges_out is not None and cfg.mode == MODE_PARITY
+    cap = 1 << 16 if want else 0
+    while True:
+        r, st = _Result(), _Stats()
+        need = C.c_int64(0)
+        words = (C.c_int32 * cap)() if cap else None
+        _check(lib().mcsg_solve_with_restarts(C.byref(g._c()), C.byref(h._c()), C.byref(o), C.byref(r),
+                                              C.byref(st), words, cap, C.byref(need)))
+        if not want or need.value <= cap:
+            break
+        cap = need.value  # the run is deterministic: again with room for every range
+    if words is not None:
+        words = words[:need.value]
+    res = _result(r, st, cfg.seed)
+    res.stats.restarts = int(st.restarts)
+    res.stats.visited_ranges = int(st.visited_ranges)
+    if cfg.mode == MODE_PARITY:
+        res.stats.recursions = int(st.nodes)
+    if words is not None:
+        w, i = words, 0
+        keys = []
+        while i < len(w):
+            k = w[i]
+            keys.append([(d, w[i + 1 + d]) for d in range(k)])
+            i += 1 + k
+        for j in range(0, len(keys), 2):
+            cfg.ranges_out.add(keys[j], keys[j + 1])
+    return res
+
+
 # ----------------------------------------------------------------- engines --
 _ORDER_NAMES = {"degree": OrderingStrategy.degree_desc,
                 "components": OrderingStrategy.components_then_degree,
@@ -696,11 +792,12 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
 
     recursive / iterative -> parity mode (reference node order);
     parallel / gpu       -> throughput mode (all warps, donation);
-    goal / jump          -> GPU goal probes; restarts:<seed> -> throughput mode
-    with that seed's search order and the reference's restart rule
-    (RestartConfig::multiplier = 2: every warp freezes its open path into
-    the ring when the nodes since the last improvement reach twice the nodes
-    at it). Orderings are applied host-side around every engine.
+    goal / jump          -> GPU goal probes; restarts:<seed> -> solve_with_restarts
+    (RestartConfig::multiplier = 2): with a parity-mode config the reference's
+    RestartDriver exactly; otherwise throughput mode with that seed's search
+    order, every warp freezing its open path into the ring when the nodes
+    since the last improvement reach twice the nodes at it. Orderings are
+    applied host-side around every engine.
     """
     import dataclasses
     cfg = dataclasses.replace(config or SolveConfig(), order=spec.order)
@@ -716,8 +813,13 @@ def run_engine(g: Graph, h: Graph, spec: EngineSpec, config: SolveConfig | None 
     if spec.goal_directed:
         return solve_goal_directed(g, h, cfg)
     if spec.restart_seed is not None:
-        return solve(g, h, dataclasses.replace(cfg, mode=MODE_THROUGHPUT, seed=spec.restart_seed,
-                                               restart_multiplier=2.0))
+        # RestartConfig from the solve config (portfolio.cpp:123-133); an
+        # explicit parity-mode config runs the reference's RestartDriver
+        # exactly, otherwise the all-warp engine's restart epochs
+        return solve_with_restarts(g, h, RestartConfig(
+            seed=spec.restart_seed, budget_seconds=cfg.budget_seconds, order=cfg.order, cancel=cfg.cancel,
+            disable_pruning=cfg.disable_pruning, shared_bound=cfg.shared_bound,
+            mode=MODE_PARITY if cfg.mode == MODE_PARITY else MODE_THROUGHPUT, device=cfg.device))
     if spec.deadend is not None:
         # forecast-then-mitigate (portfolio.cpp:136-155): a monitored solve;
         # with a jump configured, a suspect verdict hands the incumbent to the

@@ -181,6 +181,36 @@ struct Ctl {
     Line32 live;       // instances with unfinished tasks (fairness share)
 };
 
+// One segment of the exact restart engine (parity mode; RestartDriver,
+// restarts.cpp:35-191). The host keeps the segment pool as position keys —
+// the iteration taken at each step from the root, a step being a u child
+// (iteration = rank of u in the selected class's R, ascending) or the "v
+// unmatched" continuation (iteration = |R|) — and draws the next segment with
+// the reference's mt19937_64. The kernel (one warp) replays the key from the
+// root classes to the segment's node, enters it (counted, restart check,
+// offer, bound, select), resumes its branch loop at `from_iter`, and runs the
+// subtree with the reference's per-node restart check: when nodes since the
+// last improvement reach mult x max(1, nodes at that improvement) it stops at
+// that node's entry and reports the path to it (the iterations below the
+// segment's node), from which the host freezes the path into segments and
+// records the visited ranges exactly as the reference does.
+struct RxState {
+    // in
+    double mult;                   // RestartConfig::multiplier (<= 0: no restart check)
+    unsigned long long nodes0;     // nodes counted before this segment (RestartDriver::nodes)
+    unsigned long long at0;        // RestartDriver::at_improvement
+    int32_t script_len;            // steps from the root to the segment's node
+    int32_t from_iter;             // first iteration still to run at the segment's node
+    uint8_t script[kMaxWideN + 1]; // the iterations of those steps
+    // out
+    int32_t fired;                 // 1: a restart fired at the entry of the path's last node
+    int32_t log_len;               // steps below the segment's node to that node (0: the segment's node)
+    unsigned long long nodes;      // nodes counted after this segment
+    unsigned long long at;         // at_improvement after this segment (before the rearm of a restart)
+    uint8_t log[kMaxWideN + 1];    // the iterations of those steps
+    uint8_t lp_at[kMaxWideN + 2];  // kernel scratch: path length at each open level
+};
+
 constexpr int kMaxPeers = 16;
 constexpr int kMaxLadder = 32;  // probe targets of one parallel binary-search round
 
@@ -246,6 +276,9 @@ struct KernelParams {
     int32_t ladder_n;
     int32_t ladder_goal[kMaxLadder];
     GroupState* ladder_grp[kMaxLadder];
+    // Exact restart engine (parity mode, one instance): the segment to run;
+    // null otherwise.
+    RxState* rx;
 };
 
 }  // namespace mcsg

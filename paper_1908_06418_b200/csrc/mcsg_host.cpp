@@ -15,9 +15,11 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <thread>
 
 #include "../../include/mcsg.h"
@@ -90,6 +92,8 @@ struct Context {
     int32_t* h_xbest = nullptr;   // stored improvements: kernel -> host (pinned, mapped)
     int32_t* d_xbest = nullptr;
     int clock_khz = 0;            // SM clock (cycle counters -> seconds)
+    RxState* d_rx = nullptr;      // exact restart engine: the segment in flight
+    RxState* h_rx = nullptr;      // (pinned)
     std::mutex mu;
 
     explicit Context(int dev) : device(dev) {
@@ -147,6 +151,12 @@ struct Context {
             ck(cudaMalloc(&d_spill, spill), "spill");
             spill_bytes = spill;
         }
+    }
+
+    void ensure_rx() {
+        if (d_rx) return;
+        ck(cudaMalloc(&d_rx, sizeof(RxState)), "restart segment");
+        ck(cudaMallocHost(&h_rx, sizeof(RxState)), "restart segment host");
     }
 
     void reserve_wide(size_t n_inst) {
@@ -227,6 +237,7 @@ struct LaunchOut {
     int warps = 0, ctas = 0, smem_per_cta = 0, smem_classes = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
     int clock_khz = 0;
+    RxState rx{};  // exact restart engine: the segment's outcome
 };
 
 Job make_job(const HostGraph& g, const HostGraph& h, int order) {
@@ -314,6 +325,7 @@ struct LaunchExtras {
     std::vector<uint8_t> seed_v, seed_u;
     std::vector<int> ladder_goal;            // probe ladder of the round (ascending goals)
     std::vector<GroupState*> ladder_grp;     // its groups: local or peer GroupState
+    const RxState* rx = nullptr;             // exact restart engine: the segment to run (parity mode)
 };
 
 // A launch in flight on one context (ctx.mu held by the caller until finish()).
@@ -329,6 +341,7 @@ struct InFlight {
     size_t seeded = 0;
     std::chrono::steady_clock::time_point t_stage;
     double h2d_s = 0;
+    bool rx = false;
 };
 
 // Kernel shape for a batch: specialisation, shared-memory class stack, grid.
@@ -523,9 +536,20 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
         p.deadend_rel = o.deadend_rel;
     }
 
+    if (ex.rx) {
+        if (!parity || n != 1) throw Error("the exact restart engine runs one instance in parity mode");
+        ctx.ensure_rx();
+        *ctx.h_rx = *ex.rx;
+        ctx.h_rx->fired = ctx.h_rx->log_len = 0;
+        ck(cudaMemcpyAsync(ctx.d_rx, ctx.h_rx, sizeof(RxState), cudaMemcpyHostToDevice, ctx.stream), "h2d");
+        p.rx = ctx.d_rx;
+        f.rx = true;
+    }
+
     ck(cudaEventRecord(ctx.ev0, ctx.stream), "event");
     ck(kernel_launch(f.bits, f.directed, parity, p, f.ctas, ctx.stream), "search kernel launch");
     ck(cudaEventRecord(ctx.ev1, ctx.stream), "event");
+    if (f.rx) ck(cudaMemcpyAsync(ctx.h_rx, ctx.d_rx, sizeof(RxState), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_ist, ctx.d_ist, sizeof(InstanceState) * n, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_grp, ctx.d_grp, sizeof(GroupState) * n_groups, cudaMemcpyDeviceToHost, ctx.stream), "d2h");
     ck(cudaMemcpyAsync(ctx.h_cnt, ctx.d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, ctx.stream), "d2h");
@@ -575,6 +599,11 @@ LaunchOut finish(InFlight& f) {
     out.d2h_bytes = sizeof(InstanceState) * uint64_t(n) + sizeof(GroupState) * uint64_t(n_groups) +
                     sizeof(Counters) + sizeof(Ctl);
     out.launches = 2;  // ring reset + search kernel
+    if (f.rx) {
+        out.rx = *ctx.h_rx;
+        out.h2d_bytes += sizeof(RxState);
+        out.d2h_bytes += sizeof(RxState);
+    }
     if (out.counters.overflow) throw Error("class stack overflow (internal error)");
     if (out.counters.bad_task)
         throw Error("malformed subtree in the task ring (internal error): ticket " +
@@ -626,7 +655,7 @@ LaunchOut finish(InFlight& f) {
 }
 
 // The single-device launch path shared by every entry point.
-LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
+LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o, const LaunchExtras& ex = LaunchExtras{}) {
     if (jobs.empty()) {
         LaunchOut out;
         out.groups.resize(n_groups);
@@ -648,7 +677,7 @@ LaunchOut launch(std::vector<Job>& jobs, int n_groups, const mcsg_options& o) {
         ctx->mu.lock();
     }
     std::lock_guard<std::mutex> lock(ctx->mu, std::adopt_lock);
-    InFlight f = start(*ctx, jobs, n_groups, o, LaunchExtras{});
+    InFlight f = start(*ctx, jobs, n_groups, o, ex);
     return finish(f);
 }
 
@@ -951,6 +980,141 @@ Probe probe_goal(const HostGraph& g, const HostGraph& h, int goal, const mcsg_op
     return pr;
 }
 
+// ------------------------------------------------------ exact restarts --
+// RestartDriver (restarts.cpp:35-246) with the reference's semantics, for
+// parity mode: the host owns the segment pool as position keys (PositionKey,
+// heuristics.hpp:77: the iteration taken at each depth; the depth is the
+// index) and draws the next segment with the reference's seeded
+// std::mt19937_64 (restarts.cpp:213-228). Each segment is one launch of the
+// parity kernel (RxState): replay to the segment's node, resume at
+// from_iter, per-node restart check. When a restart fires the kernel reports
+// the path below the segment's node; the host then freezes it exactly as the
+// unwinding in node() does — the node where it fired first (whole, :92-95),
+// then every node on the path, deepest first, with its remaining iterations
+// (:176-186) — and records the completed prefixes as visited ranges (:182).
+// A segment that ends without a restart records its whole span (:113,119,189).
+using PosKey = std::vector<int32_t>;
+
+PosKey key_successor(const PosKey& pos) {  // restarts.cpp:13-18
+    if (pos.empty()) return {std::numeric_limits<int32_t>::max()};
+    PosKey s = pos;
+    s.back() += 1;
+    return s;
+}
+
+PosKey key_extend(const PosKey& pos, int it) {  // restarts.cpp:20-24
+    PosKey s = pos;
+    s.push_back(it);
+    return s;
+}
+
+struct RestartOut {
+    JobResult best;
+    uint64_t nodes = 0, restarts = 0;
+    std::vector<std::pair<PosKey, PosKey>> ranges;
+};
+
+RestartOut restarts_exact(const HostGraph& G, const HostGraph& H, const mcsg_options& o, mcsg_stats* st) {
+    Job job = make_job(G, H, o.order);  // with_ordering (search_core.hpp:72-81)
+    job.floor_size = o.floor_size;
+    const int ng = job.g.n, nh = job.h.n;
+    std::vector<int> fwd_g(ng), fwd_h(nh);  // original id -> searched id
+    for (int x = 0; x < ng; ++x) fwd_g[job.inv_g.empty() ? x : job.inv_g[x]] = x;
+    for (int x = 0; x < nh; ++x) fwd_h[job.inv_h.empty() ? x : job.inv_h[x]] = x;
+    const int maxp = std::min(ng, nh);
+    const bool unlimited = o.budget_s >= 1e8;
+    const auto deadline = std::chrono::steady_clock::now() +
+                          std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                              std::chrono::duration<double>(unlimited ? 0.0 : o.budget_s));
+    mcsg_options lo = o;
+    lo.mode = MCSG_MODE_PARITY;
+    lo.goal = 0;
+    lo.deadend_abs = 0;
+    lo.deadend_rel = 0;
+    lo.deadend_kind = 0;
+    lo.deadend_jump = 0;
+    lo.restart_multiplier = 0;
+    lo.n_devices = 0;
+
+    struct Segment {
+        PosKey pos;
+        int from_iter;
+    };
+    std::mt19937_64 rng(o.seed);
+    std::vector<Segment> pool{{PosKey{}, 0}};
+    RestartOut out;
+    out.best.status = MCSG_OPTIMAL;
+    uint64_t at = 0;
+    LaunchExtras ex;
+    RxState rx{};
+    ex.rx = &rx;
+    if (st) std::memset(st, 0, sizeof(*st));
+    while (!pool.empty()) {
+        const size_t idx = pool.size() == 1 ? 0 : size_t(rng() % pool.size());
+        Segment seg = std::move(pool[idx]);
+        pool.erase(pool.begin() + std::ptrdiff_t(idx));
+        if (!unlimited) {
+            lo.budget_s = std::chrono::duration<double>(deadline - std::chrono::steady_clock::now()).count();
+            if (lo.budget_s <= 0) {
+                out.best.status = MCSG_TIMEOUT;
+                break;
+            }
+        }
+        if (seg.pos.size() > sizeof(rx.script)) throw Error("restart segment deeper than the graph");
+        rx.mult = o.restart_multiplier;
+        rx.nodes0 = out.nodes;
+        rx.at0 = at;
+        rx.script_len = int32_t(seg.pos.size());
+        rx.from_iter = seg.from_iter;
+        for (size_t i = 0; i < seg.pos.size(); ++i) rx.script[i] = uint8_t(seg.pos[i]);
+        std::vector<Job> jobs{job};
+        LaunchOut r = launch(jobs, 1, lo, ex);
+        accumulate(st, r);
+        const JobResult& jr = r.jobs[0];
+        out.nodes = r.rx.nodes;
+        at = r.rx.at;
+        if (jr.size > out.best.size) {  // the incumbent travels with the next segments
+            const int status = out.best.status;
+            out.best = jr;
+            out.best.status = status;
+            ex.seed_best = jr.size;
+            ex.seed_v.assign(size_t(jr.size), 0);
+            ex.seed_u.assign(size_t(jr.size), 0);
+            for (int k = 0; k < jr.size; ++k) {
+                ex.seed_v[k] = uint8_t(fwd_g[jr.pairs[2 * k]]);
+                ex.seed_u[k] = uint8_t(fwd_h[jr.pairs[2 * k + 1]]);
+            }
+        }
+        if (jr.status != MCSG_OPTIMAL) {  // timeout / cancel: the segment is abandoned
+            out.best.status = jr.status;
+            break;
+        }
+        if (!o.disable_pruning && out.best.size >= maxp) break;  // max_reached (restarts.cpp:108-111)
+        const PosKey lo_key = seg.from_iter == 0 ? seg.pos : key_extend(seg.pos, seg.from_iter);
+        if (!r.rx.fired) {
+            out.ranges.emplace_back(lo_key, key_successor(seg.pos));
+            continue;
+        }
+        ++out.restarts;
+        at = out.nodes;  // rearm (restarts.cpp:90)
+        const int len = r.rx.log_len;
+        if (len == 0) {  // fired at the segment's own entry: frozen whole again
+            pool.push_back(std::move(seg));
+            continue;
+        }
+        std::vector<PosKey> path(size_t(len) + 1);
+        path[0] = seg.pos;
+        for (int k = 0; k < len; ++k) path[k + 1] = key_extend(path[k], r.rx.log[k]);
+        pool.push_back({path[len], 0});
+        for (int k = len - 1; k >= 0; --k) {
+            pool.push_back({path[k], int(r.rx.log[k]) + 1});
+            out.ranges.emplace_back(k == 0 ? lo_key : path[k], key_extend(path[k], r.rx.log[k]));
+        }
+    }
+    out.best.nodes = out.nodes;
+    return out;
+}
+
 }  // namespace
 }  // namespace mcsg
 
@@ -1077,6 +1241,52 @@ int32_t mcsg_solve(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options*
         return out->status;
     }
     return solve_plain(g, h, o, out, stats);
+}
+
+int32_t mcsg_solve_with_restarts(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,
+                                 mcsg_result* out, mcsg_stats* stats, int32_t* ranges_out, int64_t ranges_cap,
+                                 int64_t* ranges_len) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        const mcsg_options o = defaults(opt);
+        const HostGraph G = HostGraph::from_abi(g), H = HostGraph::from_abi(h);
+        check_pair(G, H);
+        if (ranges_len) *ranges_len = 0;
+        if (o.budget_s <= 0) {  // restarts.cpp:197-202
+            timed_out(out);
+            if (stats) std::memset(stats, 0, sizeof(*stats));
+            return MCSG_TIMEOUT;
+        }
+        if (o.mode != MCSG_MODE_PARITY) {  // the throughput engine's restart epochs
+            const int32_t rc = solve_plain(g, h, o, out, stats);
+            if (stats && rc == MCSG_OPTIMAL) stats->visited_ranges = 1;  // the whole tree, exactly once
+            return rc;
+        }
+        if (o.n_devices > 1) throw Error("parity mode runs on one device");
+        RestartOut r = restarts_exact(G, H, o, stats);
+        write_result(G, H, r.best, out);
+        if (stats) {
+            stats->nodes = r.nodes;
+            stats->restarts = r.restarts;
+            stats->visited_ranges = r.ranges.size();
+            stats->wall_s = secs_since(t0);
+        }
+        // ranges: per run [len(lo), lo..., len(hi), hi...]
+        int64_t w = 0;
+        for (const auto& run : r.ranges)
+            for (const PosKey* k : {&run.first, &run.second}) {
+                if (ranges_out && w < ranges_cap) ranges_out[w] = int32_t(k->size());
+                ++w;
+                for (int32_t x : *k) {
+                    if (ranges_out && w < ranges_cap) ranges_out[w] = x;
+                    ++w;
+                }
+            }
+        if (ranges_len) *ranges_len = w;
+        return out->status;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 int32_t mcsg_solve_parallel(const mcsg_graph* g, const mcsg_graph* h, const mcsg_options* opt,

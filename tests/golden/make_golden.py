@@ -4,7 +4,7 @@ Runs in the dev container only (needs oracle/_ref/libmcs_ref.so, built from
 /root/reference/proj/src by oracle/Makefile). The JSON fixtures it writes are
 committed; tests on the GPU box read them without the reference.
 
-    python tests/golden/make_golden.py [small|c2|c5|c3|all|c5full|c4]
+    python tests/golden/make_golden.py [small|c2|c5|c3|all|c5full|c4|restarts]
 """
 from __future__ import annotations
 
@@ -202,6 +202,48 @@ def deadend():
     dump("deadend.json", {"cases": out})
 
 
+def restarts():
+    """solve_with_restarts (restarts.cpp:195-246) through the reference's own
+    RestartConfig: seeded segment draws, recursions, restarts, visited ranges
+    (and the ranges themselves, the VisitedRanges sink, for the smaller runs).
+    The cases follow the reference's restart tests (test_heuristics.cpp:
+    131-208: random_pairs(40,4,9,454) with seed 1+13i; (10,4,6,999) eager and
+    exhaustive; (12,.5,71/72) seed 5 multiplier 1) plus config-1 pairs, orderings,
+    directed/labelled pairs and n_H > 32 / n_H > 64 shapes."""
+    cases = []
+    for i, (n, d, s) in enumerate(random_pairs(40, 4, 9, 454)):
+        cases.append(dict(n=n, d=d, seed=s, rseed=1 + 13 * i, mult=2.0, prune=True, order=0))
+    for n, d, s in random_pairs(10, 4, 6, 999):
+        cases.append(dict(n=n, d=d, seed=s, rseed=s, mult=1.0, prune=False, order=0))
+    cases.append(dict(n=12, d=0.5, seed=71, rseed=5, mult=1.0, prune=True, order=0))
+    for s in (1, 3, 5, 7, 9):
+        cases.append(dict(n=20, d=0.3, seed=s, rseed=7 * s, mult=2.0, prune=True, order=0))
+        cases.append(dict(n=20, d=0.3, seed=s, rseed=s, mult=1.0, prune=True, order=1 + s % 3))
+        cases.append(dict(n=20, d=0.3, seed=s, rseed=3, mult=0.0, prune=True, order=0))
+    for i, (n, d, s) in enumerate(random_pairs(12, 10, 16, 8080)):
+        cases.append(dict(n=n, d=d, seed=s, rseed=100 + i, mult=0.5 + 0.5 * (i % 4), prune=True, order=0,
+                          directed=i % 2 == 1, labels=(0, 2, 3)[i % 3]))
+    for i, (n, nh, d) in enumerate(((11, 36, 0.3), (12, 40, 0.5), (12, 34, 0.8), (11, 70, 0.5))):
+        # n_H > 32 / > 64: the 64-bit and 128-bit kernels
+        cases.append(dict(n=n, nh=nh, d=d, seed=9000 + i, rseed=17 + i, mult=1.0, prune=True, order=0))
+    out = []
+    for c in cases:
+        dr, lb = c.get("directed", False), c.get("labels", 0)
+        g = O.ref_random_graph(c["n"], c["d"], c["seed"], dr, lb)
+        h = O.ref_random_graph(c.get("nh", c["n"]), c["d"], c["seed"] + 1, dr, lb)
+        r = O.ref_solve_with_restarts(g, h, c["rseed"], c["mult"], c["prune"], c["order"])
+        assert r.status == 0, c
+        rec = dict(c, size=r.size, nodes=r.nodes, restarts=r.extra["restarts"],
+                   visited_ranges=r.extra["visited_ranges"], pairs=[list(p) for p in r.pairs])
+        if r.extra["visited_ranges"] <= 400:
+            rec["ranges"] = [[[x for _, x in lo], [x for _, x in hi]] for lo, hi in r.extra["ranges"]]
+        out.append(rec)
+        print("restarts", c["n"], c["d"], c["seed"], r.size, r.nodes, r.extra["restarts"],
+              r.extra["visited_ranges"], flush=True)
+    dump("restarts.json", {"cases": out, "how": "reference solve_with_restarts (oracle/_ref) with the "
+                           "VisitedRanges sink; ranges as iteration lists per key"})
+
+
 def c3_pairs():
     """C3 (BASELINE configs[2]): directed vertex-labelled ER n=40,
     L in {2,4,8} x p in {.1,.3,.5} x 10 pairs, seeds 40000+2i / 40001+2i."""
@@ -307,3 +349,5 @@ if __name__ == "__main__":
         deadend()
     if what == "c4":
         c4()
+    if what in ("restarts", "all"):
+        restarts()

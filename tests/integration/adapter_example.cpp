@@ -5,6 +5,7 @@
 #include <cstdio>
 
 #include "mcs/graph.hpp"
+#include "mcs/heuristics.hpp"
 #include "mcs/solve.hpp"
 #include "mcsg_reference_adapter.hpp"
 
@@ -26,6 +27,21 @@ int main() {
              par.best == ref.best && thr.size == ref.size && gpu::verify(g, h, thr.best);
         std::printf("gpu solve parity: %s (size %d, nodes %llu vs %llu)\n", ok ? "ok" : "FAIL", par.size,
                     (unsigned long long)par.stats.recursions, (unsigned long long)ref.stats.recursions);
+        fails += !ok;
+        // the reference's RestartDriver through the adapter: identical stats and ranges
+        RestartConfig rc;
+        rc.seed = 7;
+        rc.multiplier = 1.0;
+        VisitedRanges vr_ref, vr_gpu;
+        rc.ranges_out = &vr_ref;
+        SolveResult rref = solve_with_restarts(g, h, rc);
+        rc.ranges_out = &vr_gpu;
+        SolveResult rgpu = gpu::solve_with_restarts(g, h, rc);
+        ok = rgpu.size == rref.size && rgpu.best == rref.best && rgpu.stats.recursions == rref.stats.recursions &&
+             rgpu.stats.restarts == rref.stats.restarts && rgpu.stats.visited_ranges == rref.stats.visited_ranges &&
+             vr_gpu.runs == vr_ref.runs;
+        std::printf("gpu restarts parity: %s (restarts %llu, ranges %llu)\n", ok ? "ok" : "FAIL",
+                    (unsigned long long)rgpu.stats.restarts, (unsigned long long)rgpu.stats.visited_ranges);
         fails += !ok;
     } catch (const GraphError& e) {
         // without a device the adapter must raise, never fall back to the CPU

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
             "mcsg_bound_jump", "mcsg_portfolio", "mcsg_verify", "mcsg_load_graph_file"} <= set(syms)
     for name in syms:
         assert hasattr(lib, name), f"{name} declared in include/mcsg.h but not exported"
-    assert M.lib().mcsg_abi_version() == 4
+    assert M.lib().mcsg_abi_version() == 5
 
 
 def test_library_is_sm100a_only():

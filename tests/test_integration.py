@@ -45,4 +45,5 @@ def test_adapter_gpu_parity_through_reference_types():
         pytest.skip("adapter example not prebuilt (built by the CPU test in the dev container)")
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert "gpu solve parity: ok" in out.stdout, out.stdout + out.stderr
+    assert "gpu restarts parity: ok" in out.stdout, out.stdout + out.stderr
     assert out.returncode == 0

@@ -139,3 +139,38 @@ def test_live_reference_agreement():
             r = O.solve(g, h)
             rr = O.ref_run_engine(g, h, "recursive")
             assert (r.size, r.nodes, r.pairs) == (rr.size, rr.nodes, rr.pairs)
+
+
+def test_restarts_match_reference():
+    """solve_with_restarts restated (restarts.cpp:195-246) vs the unmodified
+    reference's (tests/golden/restarts.json): size, recursions, restarts,
+    visited ranges, mapping and the ranges themselves."""
+    cases = json.load(open(os.path.join(HERE, "golden", "restarts.json")))["cases"]
+    assert len(cases) >= 80
+    for c in cases:
+        dr, lb = c.get("directed", False), c.get("labels", 0)
+        g = O.random_graph(c["n"], c["d"], c["seed"], dr, lb)
+        h = O.random_graph(c.get("nh", c["n"]), c["d"], c["seed"] + 1, dr, lb)
+        r = O.solve_with_restarts(g, h, seed=c["rseed"], multiplier=c["mult"], prune=c["prune"], order=c["order"])
+        got = (r.status, r.size, r.nodes, r.extra["restarts"], r.extra["visited_ranges"])
+        assert got == (0, c["size"], c["nodes"], c["restarts"], c["visited_ranges"]), c
+        assert [list(p) for p in r.pairs] == c["pairs"]
+        if "ranges" in c:
+            assert [[[x for _, x in lo], [x for _, x in hi]] for lo, hi in r.extra["ranges"]] == c["ranges"]
+
+
+def test_restart_ranges_tile_the_tree():
+    """test_heuristics.cpp:177-199 on the restatement: disjoint ranges merging
+    into one run from the root key to successor({})."""
+    for n, d, s in [(4 + i % 3, (0.2, 0.5, 0.8)[i % 3], 999 + 977 * i) for i in range(10)]:
+        g, h = O.random_graph(n, d, s), O.random_graph(n, d, s + 1)
+        r = O.solve_with_restarts(g, h, seed=s, multiplier=1.0, prune=False)
+        runs = sorted((list(lo), list(hi)) for lo, hi in r.extra["ranges"])
+        merged = []
+        for lo, hi in runs:
+            assert not merged or lo >= merged[-1][1]  # disjoint
+            if merged and lo == merged[-1][1]:
+                merged[-1][1] = hi
+            else:
+                merged.append([lo, hi])
+        assert merged == [[[], [(0, 2**31 - 1)]]]

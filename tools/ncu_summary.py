@@ -28,11 +28,14 @@ out['nodes_per_launch'] = nodes
 out['stall_pct'] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -(x[1] or 0)) if v}
 out['pipes_pct'] = {k.replace('sm__inst_executed_pipe_', '').replace('.avg.pct_of_peak_sustained_active', ''): v
                     for k, v in sorted(pipes.items(), key=lambda x: -(x[1] or 0)) if v}
-# the kernel sources the profile belongs to (bench.py flags a stale profile)
-import hashlib, os
-_h = hashlib.sha1()
-_root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1908_06418_b200", "csrc")
-for _f in ("mcsg_kernel.cu", "mcsg_search.cuh", "mcsg_task_body.inc", "mcsg_device.h"):
-    _h.update(open(os.path.join(_root, _f), "rb").read())
-out['kernel_src_sha1'] = _h.hexdigest()
+# the machine code the profile belongs to: the SHA-1 of the profiled kernel's
+# SASS in the built library (bench.py recomputes it and reports
+# profile_matches_kernel); run this against the same libmcsg.so that was profiled
+import os
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from sass_key import kernel_sass_sha1, U32_THROUGHPUT  # noqa: E402
+kernel = sys.argv[3] if len(sys.argv) > 3 else U32_THROUGHPUT
+lib = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1908_06418_b200", "libmcsg.so")
+out['kernel'] = kernel
+out['kernel_sass_sha1'] = kernel_sass_sha1(lib, kernel)
 print(json.dumps(out, indent=1))
