@@ -551,6 +551,32 @@ def run_ours(args, rank, world, local_rank):
                   f"profiles/ncu_summary.json (its kernel's SASS hash is checked against the built "
                   f"library); neither HBM nor tensor cores bind (SURVEY 8(d))"),
     }
+    # the other two views of SURVEY 8(d): the algorithmic op count per node
+    # (20 + 14 S, S measured by the C oracle on C2) against the same issue roof,
+    # and shared-memory bytes per node (the GPU's own, measured with the
+    # diagnostic counters build; the algorithmic model's) against the smem roof
+    smem_peak = sms * 128 * clk_mhz * 1e6  # B/s: 128 B per SM per clock
+    trf = {}
+    tpath = os.path.join(ROOT, "profiles", "r2_smem_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            trf = json.load(f)
+    alg = trf.get("alg", {})
+    gsm = trf.get("gpu", {})
+    per_gpu = value / world
+    roofline["algorithmic_issue"] = {
+        "ops_per_node": alg.get("ops_per_node"),
+        "frac": per_gpu * alg["ops_per_node"] / peak_issue if alg.get("ops_per_node") else None,
+        "basis": "SURVEY 8(d) ops = 20 + 14 S per node, S (parent classes re-read per refinement) measured "
+                 "by the C oracle on C2 (profiles/r2_smem_traffic.json)"}
+    roofline["smem"] = {
+        "peak": smem_peak, "unit": "B/s",
+        "gpu_bytes_per_node": gsm.get("bytes_per_node"),
+        "gpu_frac": per_gpu * gsm["bytes_per_node"] / smem_peak if gsm.get("bytes_per_node") else None,
+        "alg_bytes_per_node": alg.get("bytes_per_node"),
+        "alg_frac": per_gpu * alg["bytes_per_node"] / smem_peak if alg.get("bytes_per_node") else None,
+        "basis": "smem roof = SMs x 128 B/clk x sm_max_mhz; GPU bytes/node from the class-traffic counters "
+                 "(diagnostic build, profiles/r2_smem_traffic.json), algorithmic B = 32 C + 16 S + 16"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,

@@ -139,9 +139,11 @@ typedef struct mcsg_options {
 
 typedef struct mcsg_stats {
     uint64_t nodes;          /* stats.recursions: counted search nodes */
-    uint64_t sum_classes;    /* Σ live classes over counted nodes */
-    uint64_t splits;         /* children built (filter_classes calls) */
-    uint64_t split_classes;  /* Σ parent classes read by those splits */
+    uint64_t sum_classes;    /* reserved (0) */
+    uint64_t splits;         /* children materialised (filter_classes writing a class level) */
+    uint64_t split_classes;  /* Σ classes moved through shared memory by those splits: the
+                              * child's written + the parent's reloaded at the pop back
+                              * (the shared-memory roofline's per-node bytes) */
     uint64_t donations;      /* subtrees handed to idle warps */
     uint64_t tasks;          /* tasks executed (roots + donated) */
     uint64_t spills;         /* class levels placed in the HBM spill area */

@@ -138,9 +138,11 @@ struct alignas(128) WideSlot {
 // Global counters (one set per launch), for the roofline / stats.
 struct Counters {
     unsigned long long nodes;
-    unsigned long long sum_classes;  // Σ live classes over counted nodes
-    unsigned long long splits;       // children built (filter_classes calls)
-    unsigned long long split_classes;// Σ parent classes read by those splits
+    unsigned long long sum_classes;  // reserved (0)
+    unsigned long long splits;       // children materialised (filter_classes writes a level)
+    unsigned long long split_classes;// Σ classes moved through shared memory by those
+                                     // splits: the child's written + the parent's
+                                     // reloaded at the pop back
     unsigned long long donations;
     unsigned long long tasks;
     unsigned long long spills;       // levels placed in the HBM spill area

@@ -519,10 +519,11 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.spill_classes = f.spill_classes;
     p.smem_classes = f.smem_classes;
     p.donate = parity ? 0 : 1;
-    p.poll_interval = parity ? 4096 : 256;  // 512: +0.5% on C2 but C5 explores 15% more nodes (slower incumbent sharing)
+    // (<= 512: the kernel's packed split counters rely on it)
+    p.poll_interval = parity ? 512 : 256;  // 512: +0.5% on C2 but C5 explores 15% more nodes (slower incumbent sharing)
     if (const char* e = std::getenv("MCSG_DEBUG_POLL_INTERVAL")) {  // tests / experiments only
         const int v = int(std::strtol(e, nullptr, 10));
-        if (v >= 1 && v <= 65536) p.poll_interval = v;
+        if (v >= 1 && v <= 512) p.poll_interval = v;
     }
     p.counters = ctx.d_cnt;
     if (!parity) p.restart_mult = o.restart_multiplier;

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
     const unsigned long long deadline = p.budget_ns ? t_warp0 + p.budget_ns : 0ull;
     if (lane == 0) atomicMin(&p.counters->t_start_ns, t_warp0);
 
-    if (lane == 0) s.st_nodes = s.st_splits = s.st_donations = s.st_tasks = s.st_spills = s.st_idle = s.st_busy = 0;
+    if (lane == 0)
+        s.st_nodes = s.st_splits = s.st_split_cls = s.st_donations = s.st_tasks = s.st_spills = s.st_idle = s.st_busy = 0;
     if constexpr (X::kNest) {
         if (lane == 0) s.ca.nests_smem = s.ca.nests_hbm = 0;
     }
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
         Counters* c = p.counters;
         atomicAdd(&c->nodes, s.st_nodes);
         atomicAdd(&c->splits, s.st_splits);
+        atomicAdd(&c->split_classes, s.st_split_cls);
         atomicAdd(&c->donations, s.st_donations);
         atomicAdd(&c->tasks, s.st_tasks);
         atomicAdd(&c->spills, s.st_spills);

@@ -277,7 +277,7 @@ struct WarpSmem {
     alignas(16) uint32_t pf[24];
     // per-warp counters kept out of registers (written by lane 0)
     unsigned long long polled;     // nodes of the current task counted at earlier polls
-    unsigned long long st_nodes, st_splits, st_donations, st_tasks, st_spills;
+    unsigned long long st_nodes, st_splits, st_split_cls, st_donations, st_tasks, st_spills;
     unsigned long long st_idle, st_busy;  // clock64 cycles waiting for / running tasks
     W f_cand[kMaxDepth + 1];
     uint16_t vkey[NB];
@@ -744,7 +744,7 @@ struct WideSmem {
     unsigned long long f_word[NB + 1];
     alignas(16) uint32_t pf[24];
     unsigned long long polled;
-    unsigned long long st_nodes, st_splits, st_donations, st_tasks, st_spills;
+    unsigned long long st_nodes, st_splits, st_split_cls, st_donations, st_tasks, st_spills;
     unsigned long long st_idle, st_busy;
     WSet<NW> f_cand[NB + 1];
     uint32_t vkey[NB];
