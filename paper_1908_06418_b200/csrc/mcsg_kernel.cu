@@ -72,16 +72,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
     Ctl* const ctl = p.ctl;
     const int interval = p.poll_interval;
 
-    const unsigned long long t_warp0 = globaltimer();
-    const unsigned long long deadline = p.budget_ns ? t_warp0 + p.budget_ns : 0ull;
-    if (lane == 0) atomicMin(&p.counters->t_start_ns, t_warp0);
+    {
+        const unsigned long long t_warp0 = globaltimer();
+        if (lane == 0) {
+            atomicMin(&p.counters->t_start_ns, t_warp0);
+            s.deadline = p.budget_ns ? t_warp0 + p.budget_ns : 0ull;  // (read by lane 0 at polls)
+        }
+    }
 
     if (lane == 0)
         s.st_nodes = s.st_splits = s.st_split_cls = s.st_donations = s.st_tasks = s.st_spills = s.st_idle = s.st_busy = 0;
     if constexpr (X::kNest) {
         if (lane == 0) s.ca.nests_smem = s.ca.nests_hbm = 0;
     }
-    long long t_mark = clock64();
+    if (lane == 0) s.t_mark = clock64();
     int cur_inst = -1;
     int maxp = 0, goal = 0, prune = 1, floor_sz = 0, grp = 0;
     bool stop_all = false;
@@ -148,10 +152,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
                 __nanosleep(backoff + (gw & 31) * 8);
                 if (backoff < 1024) backoff <<= 1;
             }
-            {
+            if (lane == 0) {
                 const long long t = clock64();
-                if (lane == 0) s.st_idle += (unsigned long long)(t - t_mark);
-                t_mark = t;
+                s.st_idle += (unsigned long long)(t - s.t_mark);
+                s.t_mark = t;
             }
             if (!got) break;
         }

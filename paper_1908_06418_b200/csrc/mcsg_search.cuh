@@ -279,6 +279,9 @@ struct WarpSmem {
     unsigned long long polled;     // nodes of the current task counted at earlier polls
     unsigned long long st_nodes, st_splits, st_split_cls, st_donations, st_tasks, st_spills;
     unsigned long long st_idle, st_busy;  // clock64 cycles waiting for / running tasks
+    // cold per-warp values kept out of the hot loop's registers (lane 0)
+    unsigned long long deadline;          // %globaltimer deadline (0 = none)
+    long long t_mark;                     // clock64 at the last idle/busy switch
     W f_cand[kMaxDepth + 1];
     uint16_t vkey[NB];
     uint8_t map_v[kMaxDepth + 1];  // mapping prefix below the task's root level
@@ -403,6 +406,13 @@ struct Search {
     // a level lies entirely on one side, and the hot accessors branch on it
     // so that the shared-memory case compiles to LDS/STS (not generic LD/ST).
     static constexpr bool kSpill = sizeof(W) == 8;
+    // The 32-bit kernel's class stack provably cannot overflow: a level at
+    // depth k holds at most m - k classes (disjoint non-empty L sides), so the
+    // host's m(m+1)/2 + 64 entries (plan(), mcsg_host.cpp) bound every path,
+    // and the split's overflow check is compiled out. The compacted policy
+    // (its stack is the room above an enclosing level) and the spilling
+    // kernels keep it.
+    static constexpr bool kBoundedStack = sizeof(W) == 4 && std::is_same_v<SmT, WarpSmem<W, DIR>>;
 
     __device__ __forceinline__ bool in_smem(int base) const { return !kSpill || base < cap; }
 
@@ -581,11 +591,12 @@ struct Search {
                 const W lp = LX[k] & g[pp], rp = rx & h[pp];
                 const bool keep = (lp != 0) & (rp != 0);
                 const unsigned m = __ballot_sync(kFull, keep);
-                if (keep) {
-                    const int pos = total + __popc(m & lt);
-                    q[pos] = Cls<W>{lp, rp};
-                    key = min(key, class_key<W, TOP>(lc[k][pp], Bits<W>::popc(rp), lp, pos));
-                }
+                // branch-free: every lane computes its slot and key, the kept
+                // ones store (one predicated store, no reconvergence block)
+                const int pos = total + __popc(m & lt);
+                const unsigned ck = class_key<W, TOP>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
+                if (keep) q[pos] = Cls<W>{lp, rp};
+                key = keep ? min(key, ck) : key;
                 total += __popc(m);
             }
         }
@@ -746,6 +757,8 @@ struct WideSmem {
     unsigned long long polled;
     unsigned long long st_nodes, st_splits, st_split_cls, st_donations, st_tasks, st_spills;
     unsigned long long st_idle, st_busy;
+    unsigned long long deadline;
+    long long t_mark;
     WSet<NW> f_cand[NB + 1];
     uint32_t vkey[NB];
     uint8_t map_v[NB + 1];
@@ -765,6 +778,7 @@ struct WideSearch {
     static constexpr int P = DIR ? 4 : 2;
     static constexpr int kMinBlocks = 2;
     static constexpr bool kSpill = true;
+    static constexpr bool kBoundedStack = false;
     static constexpr bool kNest = false;
     struct HParts {
         Set o, i;  // H rows of u (out; in when directed)
