@@ -77,8 +77,19 @@ __device__ __forceinline__ W set_drop_lowest(W x) { return x & (x - 1); }
 template <typename W>
 __device__ __forceinline__ W set_andnot(W a, W b) { return a & ~b; }
 // highest set bit (-1 when empty): one FLO, where the lowest costs BREV + FLO
+// highest set bit (-1 when empty): one FLO, where the lowest costs BREV + FLO
 __device__ __forceinline__ int set_top(uint32_t x) { return 31 - __clz(x); }
 __device__ __forceinline__ int set_top(uint64_t x) { return 63 - __clzll(x); }
+// the same through PTX bfind, which yields the position directly: the 31 - clz
+// form costs a subtract ptxas does not fold into the address and shift that
+// use it (C2 +2.7%). Used by the 32-bit kernel only: the same change in the
+// 64-bit kernel's compacted subtrees slows the directed C3 launch by 6%
+// (instruction-fetch bound).
+__device__ __forceinline__ int set_top_bf(uint32_t x) {
+    unsigned r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return int(r);
+}
 template <typename W>
 __device__ __forceinline__ W set_without(W x, int b) { return x & ~(W(1) << b); }
 
@@ -206,10 +217,13 @@ __device__ __forceinline__ unsigned ld_volatile_u(const uint32_t* p) {
 // highest id flipped within its 6-bit field, and the min still picks that
 // class. The fields are packed with multiply-adds (mx < 128, mn < 128,
 // tie < 64, slot < 128).
-template <typename W, bool TOP = false>
+template <typename W, bool TOP = false, bool BF = false>
 __device__ __forceinline__ unsigned class_key(int pl, int pr, W l, int slot) {
     const unsigned mx = max(pl, pr), mn = min(pl, pr);
-    const unsigned tie = TOP ? unsigned(set_top(l)) ^ 63u : unsigned(Bits<W>::ctz(l));
+    int t;
+    if constexpr (BF) t = set_top_bf(uint32_t(l));
+    else t = set_top(l);
+    const unsigned tie = TOP ? unsigned(t) ^ 63u : unsigned(Bits<W>::ctz(l));
     return ((mx * 128u + mn) * 64u + tie) * 128u + unsigned(slot);
 }
 
@@ -413,6 +427,11 @@ struct Search {
     // (its stack is the room above an enclosing level) and the spilling
     // kernels keep it.
     static constexpr bool kBoundedStack = sizeof(W) == 4 && std::is_same_v<SmT, WarpSmem<W, DIR>>;
+    // highest set bit of a vertex set (throughput mode's v and u walk)
+    __device__ static __forceinline__ int top(W x) {
+        if constexpr (kBoundedStack) return set_top_bf(uint32_t(x));
+        else return set_top(x);
+    }
 
     __device__ __forceinline__ bool in_smem(int base) const { return !kSpill || base < cap; }
 
@@ -449,7 +468,7 @@ struct Search {
             if (c < nc) {
                 const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
                 sm += unsigned(min(pl, pr));
-                if (pl) key = min(key, class_key<W, TOP>(pl, pr, L[k], c));  // L = {}: a dead class
+                if (pl) key = min(key, class_key<W, TOP, kBoundedStack>(pl, pr, L[k], c));  // L = {}: a dead class
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -594,7 +613,7 @@ struct Search {
                 // branch-free: every lane computes its slot and key, the kept
                 // ones store (one predicated store, no reconvergence block)
                 const int pos = total + __popc(m & lt);
-                const unsigned ck = class_key<W, TOP>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
+                const unsigned ck = class_key<W, TOP, kBoundedStack>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
                 if (keep) q[pos] = Cls<W>{lp, rp};
                 key = keep ? min(key, ck) : key;
                 total += __popc(m);
@@ -779,6 +798,7 @@ struct WideSearch {
     static constexpr int kMinBlocks = 2;
     static constexpr bool kSpill = true;
     static constexpr bool kBoundedStack = false;
+    __device__ static __forceinline__ int top(const Set& x) { return set_top(x); }
     static constexpr bool kNest = false;
     struct HParts {
         Set o, i;  // H rows of u (out; in when directed)
