@@ -427,6 +427,11 @@ struct Search {
     // (its stack is the room above an enclosing level) and the spilling
     // kernels keep it.
     static constexpr bool kBoundedStack = sizeof(W) == 4 && std::is_same_v<SmT, WarpSmem<W, DIR>>;
+    // cont_step updates the owner lane's registers; its shared-memory copy is
+    // next read by another lane only after a warp barrier (the split's
+    // __syncwarp before a child's level load, or the poll's before a
+    // donation), so no barrier follows the step
+    static constexpr bool kContSync = false;
     // highest set bit of a vertex set (throughput mode's v and u walk)
     __device__ static __forceinline__ int top(W x) {
         if constexpr (kBoundedStack) return set_top_bf(uint32_t(x));
@@ -443,13 +448,22 @@ struct Search {
     template <typename Ptr>
     __device__ __forceinline__ void load_from(const Ptr* p, int nc) {
         two = S > 1 && nc > 32;
+        if constexpr (kBoundedStack) {
+            // 32-bit kernel: every lane loads (a level starts at most
+            // m(m+1)/2 entries into a stack of m(m+1)/2 + 64, so slot 31 is
+            // inside it) and lanes past nc zero their class: no branch
+            const Cls<W> x = p[lane];
+            L[0] = lane < nc ? x.l : W(0);
+            R[0] = lane < nc ? x.r : W(0);
+        } else {
 #pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const int c = lane + 32 * k;
-            Cls<W> x{0, 0};
-            if (c < nc) x = p[c];
-            L[k] = x.l;
-            R[k] = x.r;
+            for (int k = 0; k < S; ++k) {
+                const int c = lane + 32 * k;
+                Cls<W> x{0, 0};
+                if (c < nc) x = p[c];
+                L[k] = x.l;
+                R[k] = x.r;
+            }
         }
     }
 
@@ -798,6 +812,7 @@ struct WideSearch {
     static constexpr int kMinBlocks = 2;
     static constexpr bool kSpill = true;
     static constexpr bool kBoundedStack = false;
+    static constexpr bool kContSync = true;  // cont_step's write is read by other lanes at once (scan_key)
     __device__ static __forceinline__ int top(const Set& x) { return set_top(x); }
     static constexpr bool kNest = false;
     struct HParts {
