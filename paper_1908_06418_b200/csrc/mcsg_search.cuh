@@ -255,6 +255,16 @@ __device__ __forceinline__ int fr_u(unsigned long long f) { return int(unsigned(
 template <typename W, bool DIR>
 struct WarpSmem;
 
+// Per-task values the DFS only needs on cold paths (offers, polls,
+// donations, the task's end), kept in shared memory (written by lane 0 at
+// task start) so that they hold no registers across the hot loop.
+struct TaskCold {
+    GroupState* gs;
+    InstanceState* is;
+    int inst, cur_inst;
+    int maxp, goal, prune, floor_sz, grp;
+};
+
 // The 64-bit kernel's area for a subtree compacted to 32 bits: a 32-bit
 // search image (rows of the live vertices, renumbered 0..31) and the maps
 // between compact and original ids.
@@ -296,6 +306,7 @@ struct WarpSmem {
     // cold per-warp values kept out of the hot loop's registers (lane 0)
     unsigned long long deadline;          // %globaltimer deadline (0 = none)
     long long t_mark;                     // clock64 at the last idle/busy switch
+    TaskCold tc;
     W f_cand[kMaxDepth + 1];
     uint16_t vkey[NB];
     uint8_t map_v[kMaxDepth + 1];  // mapping prefix below the task's root level
@@ -432,6 +443,7 @@ struct Search {
     // __syncwarp before a child's level load, or the poll's before a
     // donation), so no barrier follows the step
     static constexpr bool kContSync = false;
+    static constexpr bool kColdSmem = !(sizeof(W) == 8 && DIR);  // TaskCold in shared memory (mcsg_kernel.cu)
     // highest set bit of a vertex set (throughput mode's v and u walk)
     __device__ static __forceinline__ int top(W x) {
         if constexpr (kBoundedStack) return set_top_bf(uint32_t(x));
@@ -792,6 +804,7 @@ struct WideSmem {
     unsigned long long st_idle, st_busy;
     unsigned long long deadline;
     long long t_mark;
+    TaskCold tc;
     WSet<NW> f_cand[NB + 1];
     uint32_t vkey[NB];
     uint8_t map_v[NB + 1];
@@ -813,6 +826,7 @@ struct WideSearch {
     static constexpr bool kSpill = true;
     static constexpr bool kBoundedStack = false;
     static constexpr bool kContSync = true;  // cont_step's write is read by other lanes at once (scan_key)
+    static constexpr bool kColdSmem = true;
     __device__ static __forceinline__ int top(const Set& x) { return set_top(x); }
     static constexpr bool kNest = false;
     struct HParts {
