@@ -10,6 +10,7 @@ import os
 
 import pytest
 
+import oracle as O
 import paper_1908_06418_b200 as M
 
 pytestmark = pytest.mark.gpu
@@ -67,3 +68,19 @@ def test_heavy_donation_stress_is_exact(monkeypatch):
         assert [r.size for r in res] == [gold[str(i)] for i in range(100)]
         assert all(r.status == M.SolveStatus.optimal for r in res)
         assert st.donations > 100000
+
+
+@pytest.mark.parametrize("n,p,labels,directed", [(32, 0.5, 16, False), (32, 0.5, 32, True), (32, 0.3, 8, True)])
+def test_full_width_32bit_stacks_exhaustive(n, p, labels, directed):
+    """The 32-bit kernel's class stack carries no overflow check (its size,
+    m(m+1)/2 + 64, bounds every path: a level at depth k holds at most m - k
+    classes). Exhaustive searches on full-width n = 32 pairs with many label
+    classes reach the deepest, widest stacks: node counts must equal the
+    oracle's in parity mode and the size in throughput mode."""
+    from util import to_oracle
+    g, h = M.random_graph(n, p, 777, directed, labels), M.random_graph(n, p, 778, directed, labels)
+    o = O.solve(to_oracle(g), to_oracle(h), prune=False)
+    par = M.solve(g, h, M.SolveConfig(mode=M.MODE_PARITY, disable_pruning=True))
+    assert (par.size, par.stats.recursions) == (o.size, o.nodes)
+    thr = M.solve(g, h, M.SolveConfig(mode=M.MODE_THROUGHPUT, disable_pruning=True))
+    assert thr.status == M.SolveStatus.optimal and thr.size == o.size and M.verify(g, h, thr.best)
