@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, X::kMinBlocks)
             using CS = CompactSearch<X::kDir>;
             auto run_nested = [&](CS& xc, int nest_d, int nest_nc, int nest_sel, int nest_v, int nest_bound,
                                   uint32_t nest_cand, int nest_cont, int& cd, int& cd0, int& since_poll,
-                                  unsigned& splits, int& nest_best, int& nest_off) -> bool {
+                                  unsigned& splits, int& nest_best, int& nest_off, int nest_resume,
+                                  int& nest_pause) -> int {
                 using W = uint32_t;
                 constexpr int NB = CS::NB;
                 constexpr int P = CS::P;
