@@ -336,10 +336,10 @@ struct Search {
     static constexpr int S = Bits<W>::slots;
     static constexpr int NB = Bits<W>::n;
     static constexpr int P = DIR ? 4 : 2;  // split parts (codes 0..3 / 0..1)
-#ifndef MCSG_U64_MIN_BLOCKS
-#define MCSG_U64_MIN_BLOCKS 7  // 72 registers, 28 warps/SM: +2.6% on C4 over 6 (80 regs); 8 (64 regs) spills
-#endif
-    static constexpr int kMinBlocks = sizeof(W) == 4 ? 8 : MCSG_U64_MIN_BLOCKS;  // __launch_bounds__
+    // __launch_bounds__ CTAs/SM: the 32-bit kernel 8 (64 registers, no spill);
+    // the 64-bit kernels 7 undirected (72 registers: C4 0.8% faster than 8)
+    // and 8 directed (64 registers with some spill: C3 6% faster than 7)
+    static constexpr int kMinBlocks = sizeof(W) == 4 ? 8 : (DIR ? 8 : 7);
     // 64-bit kernel: a level whose live vertex sets fit 32 bits runs its
     // subtree compacted (CompactSearch, nested in the task) — 97% of C4's nodes
     static constexpr bool kNest = sizeof(W) == 8;
@@ -443,11 +443,15 @@ struct Search {
     // __syncwarp before a child's level load, or the poll's before a
     // donation), so no barrier follows the step
     static constexpr bool kContSync = false;
-    static constexpr bool kColdSmem = !(sizeof(W) == 8 && DIR);  // TaskCold in shared memory (mcsg_kernel.cu)
+    static constexpr bool kColdSmem = true;  // TaskCold in shared memory (mcsg_kernel.cu)
     // highest set bit of a vertex set (throughput mode's v and u walk)
     __device__ static __forceinline__ int top(W x) {
-        if constexpr (kBoundedStack) return set_top_bf(uint32_t(x));
-        else return set_top(x);
+        if constexpr (sizeof(W) == 4) return set_top_bf(uint32_t(x));
+        else {
+            unsigned r;
+            asm("bfind.u64 %0, %1;" : "=r"(r) : "l"(uint64_t(x)));
+            return int(r);
+        }
     }
 
     __device__ __forceinline__ bool in_smem(int base) const { return !kSpill || base < cap; }
@@ -494,7 +498,7 @@ struct Search {
             if (c < nc) {
                 const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
                 sm += unsigned(min(pl, pr));
-                if (pl) key = min(key, class_key<W, TOP, kBoundedStack>(pl, pr, L[k], c));  // L = {}: a dead class
+                if (pl) key = min(key, class_key<W, TOP, sizeof(W) == 4>(pl, pr, L[k], c));  // L = {}: a dead class
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -639,7 +643,7 @@ struct Search {
                 // branch-free: every lane computes its slot and key, the kept
                 // ones store (one predicated store, no reconvergence block)
                 const int pos = total + __popc(m & lt);
-                const unsigned ck = class_key<W, TOP, kBoundedStack>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
+                const unsigned ck = class_key<W, TOP, sizeof(W) == 4>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
                 if (keep) q[pos] = Cls<W>{lp, rp};
                 key = keep ? min(key, ck) : key;
                 total += __popc(m);
