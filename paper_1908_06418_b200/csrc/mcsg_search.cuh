@@ -431,13 +431,14 @@ struct Search {
     // a level lies entirely on one side, and the hot accessors branch on it
     // so that the shared-memory case compiles to LDS/STS (not generic LD/ST).
     static constexpr bool kSpill = sizeof(W) == 8;
-    // The 32-bit kernel's class stack provably cannot overflow: a level at
-    // depth k holds at most m - k classes (disjoint non-empty L sides), so the
-    // host's m(m+1)/2 + 64 entries (plan(), mcsg_host.cpp) bound every path,
-    // and the split's overflow check is compiled out. The compacted policy
-    // (its stack is the room above an enclosing level) and the spilling
-    // kernels keep it.
-    static constexpr bool kBoundedStack = sizeof(W) == 4 && std::is_same_v<SmT, WarpSmem<W, DIR>>;
+    // A 32-bit class stack provably cannot overflow: a level at depth k
+    // holds at most m - k classes (disjoint non-empty L sides), so the host's
+    // m(m+1)/2 + 64 entries (plan(), mcsg_host.cpp) bound every path of the
+    // 32-bit kernel, and a compacted subtree only starts when its room holds
+    // nc + m(m-1)/2 + 32 entries (the nest entry in mcsg_task_body.inc): the
+    // split's overflow check is compiled out, and a level load may read up to
+    // 31 entries past the level's start. The spilling kernels keep both checks.
+    static constexpr bool kBoundedStack = sizeof(W) == 4;
     // cont_step updates the owner lane's registers; its shared-memory copy is
     // next read by another lane only after a warp barrier (the split's
     // __syncwarp before a child's level load, or the poll's before a
