@@ -267,7 +267,9 @@ struct KernelParams {
     // `compact` (a small slack means a small subtree, where the compaction
     // costs more than it saves); 0 = off
     int32_t compact;
-    int32_t compact_hbm;  // the compact stack may sit in the HBM spill area (2: always, a test knob)
+    // test knob: nest only when the compact stack needs at most this many
+    // 32-bit entries (0 = no limit); larger subtrees run in the 64-bit policy
+    int32_t compact_room_cap;
     // Probe ladder (parallel binary search over goal probes):
     // every group of the launch is a probe of the same pair with its own goal,
     // and the ladder spans every device of the round. Entry k (ascending goal)

@@ -494,8 +494,8 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     // compacted subtrees (64-bit kernel): slack 3 (C4 5.3 s at 2, 5.4 at 4;
     // C3 0.55 s at 2, 0.53 at 4; every nest costs ≈ 600 warp-instructions)
     p.compact = 3;
-    p.compact_hbm = 1;
-    if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_HBM")) p.compact_hbm = int(std::strtol(e, nullptr, 10));
+    p.compact_room_cap = 0;
+    if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_ROOM")) p.compact_room_cap = int(std::strtol(e, nullptr, 10));
     if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_SLACK")) p.compact = std::max(1, int(std::strtol(e, nullptr, 10)));
     if (const char* e = std::getenv("MCSG_DEBUG_NO_COMPACT")) p.compact = (e[0] == '0') ? p.compact : 0;
     if (const char* e = std::getenv("MCSG_DEBUG_RING_WATCHDOG_NS")) p.ring_watchdog_ns = std::strtoull(e, nullptr, 10);

@@ -2,11 +2,12 @@
 
 A level whose live vertex sets fit 32 bits runs its subtree in place with the
 32-bit policy on renumbered vertices (the task body nested at that level,
-its class stack above the level in shared memory or in the HBM spill area).
-Renumbering keeps id order, so the search is the same tree: with pruning
-disabled the node count is identical with compaction on and off
-(MCSG_DEBUG_NO_COMPACT) and with the compact stack forced into shared memory
-(MCSG_DEBUG_COMPACT_HBM=0) or always into HBM (=2); optima and mappings
+its class stack above the level in shared memory; a subtree whose stack
+would not fit there runs in the 64-bit policy). Renumbering keeps id order,
+so the search is the same tree: with pruning disabled the node count is
+identical with compaction on and off (MCSG_DEBUG_NO_COMPACT) and with most
+subtrees refused for room (MCSG_DEBUG_COMPACT_ROOM=150: only small nests run
+compacted, the rest fall back to the 64-bit policy); optima and mappings
 stay exact.
 """
 import json
@@ -34,11 +35,11 @@ def test_compaction_keeps_the_exhaustive_tree(monkeypatch):
     for n, p, s, directed, labels in cases:
         g, h, go, ho = pair(n, p, s, directed, labels)
         on = _exhaustive(g, h)
-        monkeypatch.setenv("MCSG_DEBUG_COMPACT_HBM", "0")
+        monkeypatch.setenv("MCSG_DEBUG_COMPACT_ROOM", "150")
         smem = _exhaustive(g, h)
-        monkeypatch.setenv("MCSG_DEBUG_COMPACT_HBM", "2")
+        monkeypatch.setenv("MCSG_DEBUG_COMPACT_ROOM", "60")
         hbm = _exhaustive(g, h)
-        monkeypatch.delenv("MCSG_DEBUG_COMPACT_HBM")
+        monkeypatch.delenv("MCSG_DEBUG_COMPACT_ROOM")
         monkeypatch.setenv("MCSG_DEBUG_NO_COMPACT", "1")
         off = _exhaustive(g, h)
         monkeypatch.delenv("MCSG_DEBUG_NO_COMPACT")
