@@ -493,7 +493,9 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.ring_watchdog_ns = 2000000000ull;
     // compacted subtrees (64-bit kernel): slack 3 (C4 5.3 s at 2, 5.4 at 4;
     // C3 0.55 s at 2, 0.53 at 4; every nest costs ≈ 600 warp-instructions)
-    p.compact = 3;
+    // (round 2, after the nest pause: C4 4.33 / 4.24 / 4.31 s at slack 2 / 3 / 4;
+    // the directed C3 launch 0.331 / 0.342 / 0.365 s)
+    p.compact = f.directed ? 2 : 3;
     p.compact_room_cap = 0;
     if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_ROOM")) p.compact_room_cap = int(std::strtol(e, nullptr, 10));
     if (const char* e = std::getenv("MCSG_DEBUG_COMPACT_SLACK")) p.compact = std::max(1, int(std::strtol(e, nullptr, 10)));
