@@ -522,7 +522,12 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     p.smem_classes = f.smem_classes;
     p.donate = parity ? 0 : 1;
     // (<= 512: the kernel's packed split counters rely on it)
-    p.poll_interval = parity ? 512 : 256;  // 512: +0.5% on C2 but C5 explores 15% more nodes (slower incumbent sharing)
+    // Throughput mode: a launch of a few small pairs is latency bound (its
+    // tree fans out from one root: polls every 256 nodes, C1), a large or
+    // many-pair launch throughput bound (every 384 nodes: C4 -1.2%, C5 -2%,
+    // C3 -1.5%, C2 unchanged; C1 +12% at 384). tools/poll_sweep.sh.
+    const bool latency_bound = n <= 8 && f.bits == 32;
+    p.poll_interval = parity ? 512 : latency_bound ? 256 : 384;
     if (const char* e = std::getenv("MCSG_DEBUG_POLL_INTERVAL")) {  // tests / experiments only
         const int v = int(std::strtol(e, nullptr, 10));
         if (v >= 1 && v <= 512) p.poll_interval = v;
