@@ -48,6 +48,7 @@ def piece(args):
 def main():
     depth = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     workers = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    skip = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # levels whose branch pieces another run covers
     g, h = O.ref_random_graph(45, 0.5, 45000), O.ref_random_graph(45, 0.5, 45001)
     cg = np.asarray(g.codes).reshape(45, 45)
     ch = np.asarray(h.codes).reshape(45, 45)
@@ -59,7 +60,7 @@ def main():
         deg = {x: int(sum(1 for y in gl if y != x and cg[x, y])) for x in gl}
         v = min(gl, key=lambda x: (-deg[x], x))
         rest = [x for x in gl if x != v]
-        for u in range(45):
+        for u in (range(45) if level >= skip else ()):
             hrest = [y for y in range(45) if y != u]
             tasks.append((f"v{v}->u{u}@{level}", sub(g, rest, [int(cg[v, x]) for x in rest]),
                           sub(h, hrest, [int(ch[u, y]) for y in hrest]), 15))
@@ -69,15 +70,17 @@ def main():
     t0 = time.time()
     out = {"instance": "C4 ER n=45 p=0.5 seeds 45000/45001", "removed_vertices": removed, "pieces": []}
     with ProcessPoolExecutor(workers) as ex:
-        for res in ex.map(piece, tasks[::-1]):  # the big unmatched piece first
+        for res in ex.map(piece, tasks[::-1]):  # the big unmatched piece first (results print in this order)
             out["pieces"].append(res)
             print(json.dumps(res), flush=True)
     out["all_proved"] = all(p["proved"] for p in out["pieces"])
     out["nodes"] = sum(p["nodes"] for p in out["pieces"])
     out["wall_s"] = round(time.time() - t0, 1)
     out["workers"] = workers
+    out["skip_levels"] = skip
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    json.dump(out, open(os.path.join(ROOT, "gpurun_out", "c4_split_proof.json"), "w"), indent=1)
+    name = "c4_split_proof.json" if skip == 0 else f"c4_split_proof_skip{skip}.json"
+    json.dump(out, open(os.path.join(ROOT, "gpurun_out", name), "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "pieces"}))
 
 
