@@ -281,7 +281,12 @@ template <bool DIR>
 struct CompactArea {
     CompactRows<DIR> img;            // rows of the live vertices, renumbered
     uint8_t gid[32], hid[32];        // compact id -> original id
-    uint8_t cmap_g[64], cmap_h[64];  // original id -> compact id
+    // original -> compact ids: a parallel bit extract (PEXT) through the live
+    // sets, by the shift-and-mask compress of Hacker's Delight §7-4 with its
+    // five move masks per 32-bit half precomputed once per nest:
+    // mv[0..1] = G low / high half, mv[2..3] = H low / high half
+    alignas(16) uint32_t mv[4][8];
+    uint64_t lg, lh;                 // the live sets
     unsigned long long nests_smem, nests_hbm;  // subtrees run compacted, by stack placement
 };
 
@@ -699,15 +704,27 @@ struct CompactSearch : Search<uint32_t, DIR, CompactRows<DIR>> {
 
     __device__ __forceinline__ int g_orig(int v) const { return ks.ca.gid[v]; }
     __device__ __forceinline__ int h_orig(int u) const { return ks.ca.hid[u]; }
-    __device__ __forceinline__ int g_local(int v) const { return ks.ca.cmap_g[v]; }
+    __device__ __forceinline__ int g_local(int v) const { return __popcll(ks.ca.lg & ((1ull << v) - 1)); }
     __device__ __forceinline__ int stack_limit(const KernelParams&) const { return this->cap; }
 
-    // compact image of row x (⊆ the live set) through an id map
-    __device__ static __forceinline__ uint32_t compress(uint64_t x, const uint8_t* cmap) {
-        uint32_t r = 0;
-        for (uint32_t lo = uint32_t(x); lo; lo &= lo - 1) r |= 1u << cmap[__ffs(lo) - 1];
-        for (uint32_t hi = uint32_t(x >> 32); hi; hi &= hi - 1) r |= 1u << cmap[32 + __ffs(hi) - 1];
-        return r;
+    // compact image of x ⊆ the live set of side w (0 = G, 2 = H): PEXT
+    // with the nest's move masks (3 instructions per step, 5 steps per half)
+    __device__ __forceinline__ uint32_t pext(uint64_t x, int w) const {
+        uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+        const uint4 a0 = *reinterpret_cast<const uint4*>(&ks.ca.mv[w][0]);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(&ks.ca.mv[w][4]);
+        const uint4 b0 = *reinterpret_cast<const uint4*>(&ks.ca.mv[w + 1][0]);
+        const uint4 b1 = *reinterpret_cast<const uint4*>(&ks.ca.mv[w + 1][4]);
+        const uint32_t ma[5] = {a0.x, a0.y, a0.z, a0.w, a1.x};
+        const uint32_t mb[5] = {b0.x, b0.y, b0.z, b0.w, b1.x};
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const uint32_t t = lo & ma[i], u = hi & mb[i];
+            lo = (lo ^ t) | (t >> (1 << i));
+            hi = (hi ^ u) | (u >> (1 << i));
+        }
+        // a1.y = the live low half's size; the whole set has at most 32 bits
+        return lo | uint32_t(uint64_t(hi) << a1.y);
     }
 
     // Builds the compact area for live sets lg (G) and lh (H) from the
@@ -715,17 +732,34 @@ struct CompactSearch : Search<uint32_t, DIR, CompactRows<DIR>> {
     // rarely share live sets: reusing the last area hit 2% of C4's nests.)
     __device__ __forceinline__ void build(uint64_t lg, uint64_t lh) {
         const int lane = this->lane;
+        if (lane < 4) {  // the move masks of one 32-bit half per lane (HD §7-4)
+            const uint64_t mm = lane < 2 ? lg : lh;
+            uint32_t m = (lane & 1) ? uint32_t(mm >> 32) : uint32_t(mm);
+            const uint32_t n0 = __popc(m);
+            uint32_t mk = ~m << 1;
+            uint32_t o[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                uint32_t mp = mk ^ (mk << 1);
+                mp ^= mp << 2;
+                mp ^= mp << 4;
+                mp ^= mp << 8;
+                mp ^= mp << 16;
+                const uint32_t mvi = mp & m;
+                o[i] = mvi;
+                m = (m ^ mvi) | (mvi >> (1 << i));
+                mk &= ~mp;
+            }
+            *reinterpret_cast<uint4*>(&ks.ca.mv[lane][0]) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint2*>(&ks.ca.mv[lane][4]) = make_uint2(o[4], n0);
+        }
+        if (lane == 4) {
+            ks.ca.lg = lg;
+            ks.ca.lh = lh;
+        }
         for (int x = lane; x < 64; x += 32) {
-            if ((lg >> x) & 1) {
-                const int j = __popcll(lg & ((1ull << x) - 1));
-                ks.ca.gid[j] = uint8_t(x);
-                ks.ca.cmap_g[x] = uint8_t(j);
-            }
-            if ((lh >> x) & 1) {
-                const int j = __popcll(lh & ((1ull << x) - 1));
-                ks.ca.hid[j] = uint8_t(x);
-                ks.ca.cmap_h[x] = uint8_t(j);
-            }
+            if ((lg >> x) & 1) ks.ca.gid[__popcll(lg & ((1ull << x) - 1))] = uint8_t(x);
+            if ((lh >> x) & 1) ks.ca.hid[__popcll(lh & ((1ull << x) - 1))] = uint8_t(x);
         }
         __syncwarp();
         // lane j builds row j: bit k = code bit toward the k-th live vertex
@@ -734,13 +768,13 @@ struct CompactSearch : Search<uint32_t, DIR, CompactRows<DIR>> {
         uint32_t og = 0, oh = 0, ig = 0, ih = 0;
         if (lane < ng) {
             const int xg = ks.ca.gid[lane];
-            og = compress(ks.out_g[xg] & lg, ks.ca.cmap_g);
-            if constexpr (DIR) ig = compress(ks.in_g[xg] & lg, ks.ca.cmap_g);
+            og = pext(ks.out_g[xg] & lg, 0);
+            if constexpr (DIR) ig = pext(ks.in_g[xg] & lg, 0);
         }
         if (lane < nh) {
             const int xh = ks.ca.hid[lane];
-            oh = compress(ks.out_h[xh] & lh, ks.ca.cmap_h);
-            if constexpr (DIR) ih = compress(ks.in_h[xh] & lh, ks.ca.cmap_h);
+            oh = pext(ks.out_h[xh] & lh, 2);
+            if constexpr (DIR) ih = pext(ks.in_h[xh] & lh, 2);
         }
         img.out_g[lane] = og;
         img.out_h[lane] = oh;
@@ -751,16 +785,8 @@ struct CompactSearch : Search<uint32_t, DIR, CompactRows<DIR>> {
         __syncwarp();
     }
 
-    __device__ __forceinline__ uint32_t pack_g(uint64_t x) const {
-        uint32_t r = 0;
-        for (; x; x &= x - 1) r |= 1u << ks.ca.cmap_g[__ffsll(x) - 1];
-        return r;
-    }
-    __device__ __forceinline__ uint32_t pack_h(uint64_t x) const {
-        uint32_t r = 0;
-        for (; x; x &= x - 1) r |= 1u << ks.ca.cmap_h[__ffsll(x) - 1];
-        return r;
-    }
+    __device__ __forceinline__ uint32_t pack_g(uint64_t x) const { return pext(x, 0); }
+    __device__ __forceinline__ uint32_t pack_h(uint64_t x) const { return pext(x, 2); }
     __device__ __forceinline__ uint64_t unpack_g(uint32_t x) const {
         uint64_t r = 0;
         for (; x; x &= x - 1) r |= 1ull << ks.ca.gid[__ffs(x) - 1];

@@ -90,6 +90,25 @@ def test_wide_kernel_parity(n, p, seed, directed, labels):
     assert t.size == o.size and M.verify(g, h, t.best)
 
 
+@pytest.mark.parametrize("n,k,p,directed,seed", [(48, 40, 0.5, False, 21), (64, 36, 0.4, True, 22),
+                                                 (64, 60, 0.5, False, 23), (40, 34, 0.7, True, 24)])
+def test_more_than_32_classes_parity(n, k, p, directed, seed):
+    """Levels of more than 32 label classes: every one of k > 32 vertex labels
+    sits on both sides, so the 64-bit policy's second class slot (classes
+    32..63 of a level) is live from the root down."""
+    rng = np.random.default_rng(seed)
+    gr, hr = M.random_graph(n, p, seed, directed), M.random_graph(n, p, seed + 1, directed)
+    lg = rng.permutation(np.arange(n) % k).astype(np.int32)
+    lh = rng.permutation(np.arange(n) % k).astype(np.int32)
+    g, h = M.Graph(n, gr.codes, directed, lg), M.Graph(n, hr.codes, directed, lh)
+    go, ho = to_oracle(g), to_oracle(h)
+    o = O.solve(go, ho, budget=60)
+    assert o.status == 0
+    _same(M.solve(g, h, PARITY), o)
+    t = M.solve(g, h, THROUGHPUT)
+    assert t.size == o.size and M.verify(g, h, t.best)
+
+
 def test_directed_labelled_n40_parity():
     # config 3 shape (directed, vertex-labelled, n=40), easy cells
     for i, (L, p) in enumerate([(4, 0.3), (8, 0.5), (8, 0.3), (4, 0.5)]):
