@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import json
 import os
+import subprocess
 import sys
 import time
 from concurrent.futures import ProcessPoolExecutor
@@ -310,23 +311,19 @@ def c5_full(count=10000):
                                   "pairs it does not prove in 120 s go to solve_parallel"})
 
 
-def c4(floor=16, budget=6 * 3600.0):
-    """C4 (n=45, p=0.5, seeds 45000/45001): the reference pool with a size floor of
-    `floor` (SolveConfig::shared_bound). Optimal status proves no mapping of
-    size floor+1 exists; the GPU's 16-mapping, accepted by the reference's
-    oracle::verify (tests/test_gpu_golden.py), proves 16 is reached."""
-    g, h = O.ref_random_graph(45, 0.5, 45000), O.ref_random_graph(45, 0.5, 45001)
-    t0 = time.time()
-    r = O.ref_solve_parallel_floor(g, h, floor, workers=0, part_level=5, budget=budget)
-    out = {"instance": "ER n=45 p=0.5 seeds 45000/45001", "floor": floor, "status": r.status,
-           "pool_size_found": r.size, "pool_nodes": r.nodes, "wall_s": round(time.time() - t0, 1),
-           "workers": O.ref_lib().ref_hardware_concurrency(),
-           "how": "reference solve_parallel(workers=hardware_concurrency, part_level=5) with "
-                  "SharedBound floor; status 0 = no common subgraph larger than floor"}
-    print(out, flush=True)
-    assert r.status == 0, out
-    out["optimum"] = floor
-    dump("c4_proof.json", out)
+def c4():
+    """C4 (n=45, p=0.5, seeds 45000/45001). The reference pool with a floor of
+    16 timed out after 6 h (its part_level-5 tail ran on one thread), so the
+    proof of "no 17" runs the reference's own sequential solve() with a
+    SharedBound floor on each of the 541 pieces of a decomposition at the top
+    of its search tree, in parallel and resumably (tools/c4_split_proof.py ->
+    tests/golden/c4_pieces.jsonl); tools/c4_proof_json.py adds the GPU's
+    16-mapping accepted by the reference's oracle::verify and writes
+    c4_proof.json (tests/test_c4_proof.py checks the decomposition identity
+    and the ledger's coverage)."""
+    here = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    subprocess.run([sys.executable, os.path.join(here, "tools", "c4_split_proof.py"), "12"], check=True)
+    subprocess.run([sys.executable, os.path.join(here, "tools", "c4_proof_json.py"), "12"], check=True)
 
 
 if __name__ == "__main__":

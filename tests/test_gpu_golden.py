@@ -103,11 +103,12 @@ def test_c3_all_90_pairs_match_reference_pool():
 
 
 def test_c4_hard_pair_matches_reference_proof():
-    """C4 (n=45, p=0.5, seeds 45000/45001). The reference pool, seeded with a
-    size floor of 16 (SolveConfig::shared_bound), proved that no common
-    subgraph of 17 exists (tests/golden/c4_proof.json, make_golden.py c4 /
-    tools/c4_floor_reference.py); the witness of 16 recorded there was
-    accepted by the reference's own oracle::verify. The GPU must prove the
+    """C4 (n=45, p=0.5, seeds 45000/45001). The reference's own solve(), with
+    a SharedBound floor on each of the 541 pieces of a decomposition at the
+    top of its search tree, proved that no common subgraph of 17 exists
+    (tests/golden/c4_proof.json, c4_pieces.jsonl, tools/c4_split_proof.py);
+    the witness of 16 recorded there was accepted by the reference's own
+    oracle::verify. The GPU must prove the
     same optimum twice, independently: the all-warp solve, and goal probes
     (16 reachable, 17 not)."""
     path = os.path.join(HERE, "golden", "c4_proof.json")
