@@ -290,6 +290,17 @@ struct CompactArea {
     unsigned long long nests_smem, nests_hbm;  // subtrees run compacted, by stack placement
 };
 
+// 64-bit kernel: a level of more than 32 classes keeps classes 32..63 (its
+// second slot) in its stack copy, not in registers; the policy reads them
+// through this (rare: none of C3's or C4's levels have more than 32 classes
+// outside labelled roots), so the hot loop holds one class per lane.
+template <typename W>
+struct HiSlot {
+    Cls<W>* lvl;  // the current level's classes (shared memory or the HBM spill area)
+    int nc, v, sel;
+};
+struct NoHiSlot {};
+
 // Per-warp shared-memory image; the class stack follows it.
 template <typename W, bool DIR>
 struct WarpSmem {
@@ -318,6 +329,7 @@ struct WarpSmem {
     uint8_t map_u[kMaxDepth + 1];
     // 64-bit kernel only: a subtree compacted to 32 bits (CompactSearch)
     [[no_unique_address]] std::conditional_t<sizeof(W) == 8, CompactArea<DIR>, NoCompactArea> ca;
+    [[no_unique_address]] std::conditional_t<sizeof(W) == 8, HiSlot<W>, NoHiSlot> hi;
 };
 
 // Per-warp shared memory of a search policy X: its fixed image, then the
@@ -341,10 +353,12 @@ struct Search {
     static constexpr int S = Bits<W>::slots;
     static constexpr int NB = Bits<W>::n;
     static constexpr int P = DIR ? 4 : 2;  // split parts (codes 0..3 / 0..1)
-    // __launch_bounds__ CTAs/SM: the 32-bit kernel 8 (64 registers, no spill);
-    // the 64-bit kernels 7 undirected (72 registers: C4 0.8% faster than 8)
-    // and 8 directed (64 registers with some spill: C3 6% faster than 7)
-    static constexpr int kMinBlocks = sizeof(W) == 4 ? 8 : (DIR ? 8 : 7);
+    // __launch_bounds__ CTAs/SM: 8 for every flavour, 64 registers. The
+    // 64-bit kernels hold one class per lane in registers (a second slot
+    // lives in the level's stack copy, HiSlot): the undirected one then fits
+    // 64 registers with an 8-byte spill (C4 3.97 -> 3.62 s against 7 CTAs at
+    // 72 registers), the directed one spills less than with two slots (C3 -3%)
+    static constexpr int kMinBlocks = 8;
     // 64-bit kernel: a level whose live vertex sets fit 32 bits runs its
     // subtree compacted (CompactSearch, nested in the task) — 97% of C4's nodes
     static constexpr bool kNest = sizeof(W) == 8;
@@ -364,15 +378,39 @@ struct Search {
     int lane;
     unsigned lt;
 
-    // class (lane + 32*k) of the current level
-    W L[S], R[S];
-    W LX[S];        // L with the branching vertex v removed
-    int lc[S][P];   // |LX ∩ part_q(v)|
-    int rs[S];      // |R| minus 1 on the selected class (u leaves exactly that class)
+    // class `lane` of the current level (classes 32..63 of a 64-bit level:
+    // HiSlot, read from the level's stack copy)
+    W L[1], R[1];
+    W LX[1];        // L with the branching vertex v removed
+    int lc[1][P];   // |LX ∩ part_q(v)|
+    int rs[1];      // |R| minus 1 on the selected class (u leaves exactly that class)
     bool two = false;  // 64-bit kernel: the level has classes in the second slot (nc > 32)
 
-    // slot k holds live classes (slot 0 always; slot 1 only when nc > 32)
-    __device__ __forceinline__ bool live(int k) const { return k == 0 || two; }
+    // the second slot's class of this lane (lane + 32), from the stack copy,
+    // with its prep_v values (LX, per-part left counts, rs) recomputed
+    struct HiCls {
+        W lx, r;
+        int lc[P];
+        int rs;
+    };
+    __device__ __forceinline__ HiCls hi_cls(const W g[P]) const {
+        HiCls o;
+        const int c = lane + 32;
+        Cls<W> x{0, 0};
+        if (c < s.hi.nc) x = s.hi.lvl[c];
+        o.lx = x.l & ~(W(1) << s.hi.v);
+        o.r = x.r;
+        o.rs = Bits<W>::popc(x.r) - (c == s.hi.sel ? 1 : 0);
+        if constexpr (!DIR) {
+            const int a = Bits<W>::popc(o.lx & g[1]);
+            o.lc[1] = a;
+            o.lc[0] = Bits<W>::popc(o.lx) - a;
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) o.lc[q] = Bits<W>::popc(o.lx & g[q]);
+        }
+        return o;
+    }
 
     __device__ __forceinline__ Search(Sm& s_, Cls<W>* scls_, Cls<W>* gcls_, int cap_, int lane_, unsigned lt_)
         : s(s_), scls(scls_), gcls(gcls_), cap(cap_), lane(lane_), lt(lt_) {}
@@ -478,13 +516,15 @@ struct Search {
             L[0] = lane < nc ? x.l : W(0);
             R[0] = lane < nc ? x.r : W(0);
         } else {
-#pragma unroll
-            for (int k = 0; k < S; ++k) {
-                const int c = lane + 32 * k;
-                Cls<W> x{0, 0};
-                if (c < nc) x = p[c];
-                L[k] = x.l;
-                R[k] = x.r;
+            Cls<W> x{0, 0};
+            if (lane < nc) x = p[lane];
+            L[0] = x.l;
+            R[0] = x.r;
+            if constexpr (S > 1) {
+                if (two) {  // (uniform stores)
+                    s.hi.lvl = const_cast<Cls<W>*>(reinterpret_cast<const Cls<W>*>(p));
+                    s.hi.nc = nc;
+                }
             }
         }
     }
@@ -498,13 +538,20 @@ struct Search {
     template <bool TOP>
     __device__ __forceinline__ unsigned scan_key(int nc, unsigned* sum) const {
         unsigned key = kNoKey, sm = 0;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            const int c = lane + 32 * k;
-            if (c < nc) {
-                const int pl = Bits<W>::popc(L[k]), pr = Bits<W>::popc(R[k]);
-                sm += unsigned(min(pl, pr));
-                if (pl) key = min(key, class_key<W, TOP, sizeof(W) == 4>(pl, pr, L[k], c));  // L = {}: a dead class
+        if (lane < nc) {
+            const int pl = Bits<W>::popc(L[0]), pr = Bits<W>::popc(R[0]);
+            sm += unsigned(min(pl, pr));
+            if (pl) key = min(key, class_key<W, TOP, sizeof(W) == 4>(pl, pr, L[0], lane));  // L = {}: a dead class
+        }
+        if constexpr (S > 1) {
+            if (two) {
+                const int c = lane + 32;
+                if (c < nc) {
+                    const Cls<W> x = s.hi.lvl[c];
+                    const int pl = Bits<W>::popc(x.l), pr = Bits<W>::popc(x.r);
+                    sm += unsigned(min(pl, pr));
+                    if (pl) key = min(key, class_key<W, TOP, sizeof(W) == 4>(pl, pr, x.l, c));
+                }
             }
         }
         if (sum) *sum = __reduce_add_sync(kFull, sm);
@@ -522,21 +569,20 @@ struct Search {
         return int(__reduce_min_sync(kFull, k) & 63u);
     }
 
+    // (c is warp-uniform)
     __device__ __forceinline__ W class_l(int c) const {
-        if constexpr (S == 1) {
-            return __shfl_sync(kFull, L[0], c);
-        } else {
-            const W a = __shfl_sync(kFull, L[0], c & 31), b = __shfl_sync(kFull, L[1], c & 31);
-            return c < 32 ? a : b;
+        if constexpr (S > 1) {
+            if (c >= 32) return s.hi.lvl[c].l;
+            return __shfl_sync(kFull, L[0], c & 31);
         }
+        return __shfl_sync(kFull, L[0], c);
     }
     __device__ __forceinline__ W class_r(int c) const {
-        if constexpr (S == 1) {
-            return __shfl_sync(kFull, R[0], c);
-        } else {
-            const W a = __shfl_sync(kFull, R[0], c & 31), b = __shfl_sync(kFull, R[1], c & 31);
-            return c < 32 ? a : b;
+        if constexpr (S > 1) {
+            if (c >= 32) return s.hi.lvl[c].r;
+            return __shfl_sync(kFull, R[0], c & 31);
         }
+        return __shfl_sync(kFull, R[0], c);
     }
 
     __device__ __forceinline__ void g_parts(int v, W g[P]) const {
@@ -572,23 +618,20 @@ struct Search {
         W g[P];
         g_parts(v, g);
         const W vb = W(1) << v;
+        LX[0] = L[0] & ~vb;
+        rs[0] = Bits<W>::popc(R[0]) - (lane == sel ? 1 : 0);
+        if constexpr (!DIR) {
+            const int a = Bits<W>::popc(LX[0] & g[1]);
+            lc[0][1] = a;
+            lc[0][0] = Bits<W>::popc(LX[0]) - a;
+        } else {
 #pragma unroll
-        for (int k = 0; k < S; ++k) {
-            LX[k] = L[k] & ~vb;
-            if (!live(k)) {
-#pragma unroll
-                for (int q = 0; q < P; ++q) lc[k][q] = 0;
-                rs[k] = 0;
-                continue;
-            }
-            rs[k] = Bits<W>::popc(R[k]) - (lane + 32 * k == sel ? 1 : 0);
-            if constexpr (!DIR) {
-                const int a = Bits<W>::popc(LX[k] & g[1]);
-                lc[k][1] = a;
-                lc[k][0] = Bits<W>::popc(LX[k]) - a;
-            } else {
-#pragma unroll
-                for (int q = 0; q < P; ++q) lc[k][q] = Bits<W>::popc(LX[k] & g[q]);
+            for (int q = 0; q < P; ++q) lc[0][q] = Bits<W>::popc(LX[0] & g[q]);
+        }
+        if constexpr (S > 1) {
+            if (two) {  // (uniform stores)
+                s.hi.v = v;
+                s.hi.sel = sel;
             }
         }
     }
@@ -600,25 +643,33 @@ struct Search {
     __device__ __forceinline__ unsigned child_sum(int u, const HParts& hp) const {
         (void)u;
         const W* h = hp.h;
-        unsigned sm = 0;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            if (!live(k)) continue;
-            if constexpr (!DIR) {
-                const int b = Bits<W>::popc(R[k] & h[1]);
-                sm += unsigned(min(lc[k][0], rs[k] - b) + min(lc[k][1], b));
-            } else {
-                int rest = rs[k];
-#pragma unroll
-                for (int q = 1; q < P; ++q) {
-                    const int b = Bits<W>::popc(R[k] & h[q]);
-                    rest -= b;
-                    sm += unsigned(min(lc[k][q], b));
-                }
-                sm += unsigned(min(lc[k][0], rest));
+        unsigned sm = part_sum(R[0], lc[0], rs[0], h);
+        if constexpr (S > 1) {
+            if (two) {
+                W g[P];
+                g_parts(s.hi.v, g);
+                const HiCls x = hi_cls(g);
+                sm += part_sum(x.r, x.lc, x.rs, h);
             }
         }
         return __reduce_add_sync(kFull, sm);
+    }
+    __device__ static __forceinline__ unsigned part_sum(W r, const int lcq[P], int rsq, const W* h) {
+        unsigned sm = 0;
+        if constexpr (!DIR) {
+            const int b = Bits<W>::popc(r & h[1]);
+            sm += unsigned(min(lcq[0], rsq - b) + min(lcq[1], b));
+        } else {
+            int rest = rsq;
+#pragma unroll
+            for (int q = 1; q < P; ++q) {
+                const int b = Bits<W>::popc(r & h[q]);
+                rest -= b;
+                sm += unsigned(min(lcq[q], b));
+            }
+            sm += unsigned(min(lcq[0], rest));
+        }
+        return sm;
     }
 
     // filter_classes (label_classes.cpp:80-108): split every class by the
@@ -637,26 +688,32 @@ struct Search {
         const W ub = W(1) << u;
         int total = 0;
         unsigned key = kNoKey;
-#pragma unroll
-        for (int k = 0; k < S; ++k) {
-            if (!live(k)) continue;
-            const W rx = R[k] & ~ub;
-#pragma unroll
-            for (int pp = 0; pp < P; ++pp) {
-                const W lp = LX[k] & g[pp], rp = rx & h[pp];
-                const bool keep = (lp != 0) & (rp != 0);
-                const unsigned m = __ballot_sync(kFull, keep);
-                // branch-free: every lane computes its slot and key, the kept
-                // ones store (one predicated store, no reconvergence block)
-                const int pos = total + __popc(m & lt);
-                const unsigned ck = class_key<W, TOP, sizeof(W) == 4>(lc[k][pp], Bits<W>::popc(rp), lp, pos);
-                if (keep) q[pos] = Cls<W>{lp, rp};
-                key = keep ? min(key, ck) : key;
-                total += __popc(m);
+        split_parts<TOP>(LX[0], R[0] & ~ub, lc[0], g, h, q, total, key);
+        if constexpr (S > 1) {
+            if (two) {
+                const HiCls x = hi_cls(g);
+                split_parts<TOP>(x.lx, x.r & ~ub, x.lc, g, h, q, total, key);
             }
         }
         *key_out = __reduce_min_sync(kFull, key);
         return total;
+    }
+    template <bool TOP>
+    __device__ __forceinline__ void split_parts(W lx, W rx, const int lcq[P], const W g[P], const W h[P], Cls<W>* q,
+                                                int& total, unsigned& key) const {
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) {
+            const W lp = lx & g[pp], rp = rx & h[pp];
+            const bool keep = (lp != 0) & (rp != 0);
+            const unsigned m = __ballot_sync(kFull, keep);
+            // branch-free: every lane computes its slot and key, the kept
+            // ones store (one predicated store, no reconvergence block)
+            const int pos = total + __popc(m & lt);
+            const unsigned ck = class_key<W, TOP, sizeof(W) == 4>(lcq[pp], Bits<W>::popc(rp), lp, pos);
+            if (keep) q[pos] = Cls<W>{lp, rp};
+            key = keep ? min(key, ck) : key;
+            total += __popc(m);
+        }
     }
 
     // "v unmatched" (search_core.hpp:201-212): the bound drops by
@@ -668,12 +725,14 @@ struct Search {
     __device__ __forceinline__ void cont_step(int sel, int cbits, int base, int& bound) {
         bound -= (cbits & kContDec) ? 1 : 0;
         Cls<W>* lvl = at(base);
-#pragma unroll
-        for (int k = 0; k < S; ++k)
-            if (lane + 32 * k == sel) {
-                L[k] = LX[k];
-                lvl[sel].l = LX[k];
-            }
+        if (lane == sel) {
+            L[0] = LX[0];
+            lvl[sel].l = LX[0];
+        }
+        if constexpr (S > 1) {
+            // second slot: its owner lane (the one that reads it back) writes
+            if (lane + 32 == sel) lvl[sel].l &= ~(W(1) << s.hi.v);
+        }
     }
 };
 
