@@ -478,7 +478,8 @@ struct Search {
     // holds at most m - k classes (disjoint non-empty L sides), so the host's
     // m(m+1)/2 + 64 entries (plan(), mcsg_host.cpp) bound every path of the
     // 32-bit kernel, and a compacted subtree only starts when its room holds
-    // nc + m(m-1)/2 + 32 entries (the nest entry in mcsg_task_body.inc): the
+    // nc + s0(s0-1)/2 + 32 entries, s0 = min(m, the level's Σ min) (the nest
+    // entry in mcsg_task_body.inc): the
     // split's overflow check is compiled out, and a level load may read up to
     // 31 entries past the level's start. The spilling kernels keep both checks.
     static constexpr bool kBoundedStack = sizeof(W) == 4;
@@ -743,8 +744,9 @@ struct Search {
 // ids, picks the same vertex and class as the 64-bit policy would). Rows are
 // rebuilt for the live vertices (CompactArea), the class stack is the 64-bit
 // stack's free memory above the enclosing level, seen as 8-byte classes (at
-// most nc + m(m-1)/2 + 32 of them for m = min(|∪L|, |∪R|) and the enclosing
-// level's nc entries, dead ones included), and ids are mapped back wherever
+// most nc + s0(s0-1)/2 + 32 of them for the enclosing level's nc entries,
+// dead ones included, and s0 = min(|∪L|, |∪R|, Σ min(|L|,|R|)): a nested level
+// k matches deep holds at most s0 - k classes), and ids are mapped back wherever
 // they leave the subtree: offered mappings, donated subtrees (in the 64-bit
 // format, so any warp can take them).
 template <bool DIR>
