@@ -1,6 +1,6 @@
 """A/B of library builds on one GPU (dev tool): C2 batch (bench workload),
 C3 batch, C4 proof; each lib loaded in its own process via MCSG_LIB.
-usage: python tools/ab.py LIB1.so LIB2.so ... [--reps N] [--only c2,c3,c4]"""
+usage: python tools/ab.py LIB1.so LIB2.so ... [--reps N] [--only c2,c3,c4,c5]"""
 import json, os, subprocess, sys
 
 libs = [a for a in sys.argv[1:] if a.endswith(".so")]
@@ -40,6 +40,19 @@ if "c3" in only:
     res, st = M.solve_batch(pairs, thr)
     out["c3_s"] = round(st.kernel_seconds, 4)
     out["c3_gnps"] = round(st.recursions / st.kernel_seconds / 1e9, 3)
+if "c5" in only:
+    pairs = []
+    for i in range(10000):
+        n, p = 16 + (i // 3) % 9, (0.1, 0.3, 0.5)[i % 3]
+        pairs.append((M.random_graph(n, p, 50000 + 2 * i), M.random_graph(n, p, 50001 + 2 * i)))
+    M.solve_batch(pairs, thr)
+    best = None
+    for _ in range(3):
+        res, st = M.solve_batch(pairs, thr)
+        if best is None or st.kernel_seconds < best[0]:
+            best = (st.kernel_seconds, st.recursions)
+    out["c5_s"] = round(best[0], 4)
+    out["c5_gnps"] = round(best[1] / best[0] / 1e9, 3)
 if "c4" in only:
     g, h = M.random_graph(45, 0.5, 45000), M.random_graph(45, 0.5, 45001)
     r = M.solve(g, h, M.SolveConfig(mode=M.MODE_THROUGHPUT, budget_seconds=60))
