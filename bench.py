@@ -382,7 +382,8 @@ def side_configs(M, args, rank, world, ndev, device, barrier, max_over_ranks, su
                          "peer_pushes": r.stats.peer_pushes,
                          "mapping_verified": bool(M.verify(g, h, r.best)),
                          "golden_ok": (r.size == opt) if opt is not None else None,
-                         "golden": "c4_proof.json (reference pool: no 17 with floor 16; GPU 16-mapping "
+                         "golden": "c4_proof.json (reference solve() with a size floor on each of the 541 pieces of a "
+                                   "decomposition of its tree: no 17; GPU 16-mapping "
                                    "accepted by the reference verify)" if proof else None}
             # one member per GPU (two on one GPU): orderings race in one launch
             # spread over their GPUs; restarts / dead-end members are engines
