@@ -35,6 +35,18 @@ if which in ("all", "u32"):
 if which in ("all", "u64"):
     check("u64_compact", [(M.random_graph(40, 0.3, 40000 + 2 * i, True, 4), M.random_graph(40, 0.3, 40001 + 2 * i, True, 4))
                           for i in range(2)])
+if which in ("all", "u64u"):
+    # the undirected 64-bit kernel (C4's): compacted subtrees in shared memory
+    # (PEXT entry, s0 room bound), and a level of more than 32 classes (the
+    # second class slot read from the stack copy, HiSlot)
+    import numpy as np
+    pairs = [(M.random_graph(36, 0.5, 46000 + 2 * i, False, 4), M.random_graph(36, 0.5, 46001 + 2 * i, False, 4))
+             for i in range(2)]
+    rng = np.random.default_rng(7)
+    gr, hr = M.random_graph(48, 0.5, 21), M.random_graph(48, 0.5, 22)
+    pairs.append((M.Graph(48, gr.codes, False, rng.permutation(np.arange(48) % 40).astype(np.int32)),
+                  M.Graph(48, hr.codes, False, rng.permutation(np.arange(48) % 40).astype(np.int32))))
+    check("u64_undirected", pairs)
 if which in ("all", "rst"):
     check("u32_restarts", [(M.random_graph(22, 0.4, 7), M.random_graph(22, 0.4, 8))], restart_multiplier=2.0)
 if which in ("all", "wide"):
