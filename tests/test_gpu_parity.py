@@ -109,6 +109,23 @@ def test_more_than_32_classes_parity(n, k, p, directed, seed):
     assert t.size == o.size and M.verify(g, h, t.best)
 
 
+def test_more_than_32_classes_under_heavy_donation(monkeypatch):
+    """The same >32-class levels while every warp donates and takes subtrees
+    (16-node polls): donated levels carry the second slot's classes through
+    the ring and back into HiSlot."""
+    monkeypatch.setenv("MCSG_DEBUG_POLL_INTERVAL", "16")
+    for n, k, p, directed, seed in [(48, 40, 0.5, False, 21), (64, 36, 0.4, True, 22), (56, 44, 0.6, False, 25)]:
+        rng = np.random.default_rng(seed)
+        gr, hr = M.random_graph(n, p, seed, directed), M.random_graph(n, p, seed + 1, directed)
+        g = M.Graph(n, gr.codes, directed, rng.permutation(np.arange(n) % k).astype(np.int32))
+        h = M.Graph(n, hr.codes, directed, rng.permutation(np.arange(n) % k).astype(np.int32))
+        o = O.solve(to_oracle(g), to_oracle(h), budget=60)
+        assert o.status == 0
+        t = M.solve(g, h, M.SolveConfig(mode=M.MODE_THROUGHPUT, max_warps=64))
+        assert t.status == M.SolveStatus.optimal and t.size == o.size and M.verify(g, h, t.best)
+        assert t.stats.donations > 0
+
+
 def test_directed_labelled_n40_parity():
     # config 3 shape (directed, vertex-labelled, n=40), easy cells
     for i, (L, p) in enumerate([(4, 0.3), (8, 0.5), (8, 0.3), (4, 0.5)]):
