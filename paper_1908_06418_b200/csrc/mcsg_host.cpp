@@ -524,10 +524,12 @@ InFlight start(Context& ctx, std::vector<Job>& jobs, int n_groups, const mcsg_op
     // (<= 512: the kernel's packed split counters rely on it)
     // Throughput mode: a launch of a few small pairs is latency bound (its
     // tree fans out from one root: polls every 256 nodes, C1), a large or
-    // many-pair launch throughput bound (every 384 nodes: C4 -1.2%, C5 -2%,
-    // C3 -1.5%, C2 unchanged; C1 +12% at 384). tools/poll_sweep.sh.
+    // many-pair launch throughput bound (every 512 nodes with the final
+    // kernels: C4 -0.5%, C2 / C5 +0.3%, C3 unchanged against 384, which
+    // had beaten 256 by 1-2% on C3-C5; C1 +12% at 384). tools/poll_sweep.sh,
+    // tools/gpu_call_poll9.sh, tools/gpu_call_env64.sh.
     const bool latency_bound = n <= 8 && f.bits == 32;
-    p.poll_interval = parity ? 512 : latency_bound ? 256 : 384;
+    p.poll_interval = parity ? 512 : latency_bound ? 256 : 512;
     if (const char* e = std::getenv("MCSG_DEBUG_POLL_INTERVAL")) {  // tests / experiments only
         const int v = int(std::strtol(e, nullptr, 10));
         if (v >= 1 && v <= 512) p.poll_interval = v;
