@@ -356,11 +356,13 @@ struct Search {
     // __launch_bounds__ CTAs/SM. The 32-bit kernel: 9 (56 registers, no
     // spill in the undirected kernels; 36 warps/SM: C2 +3.2%, C5 +3% against
     // 8 at 64 registers; 10 at 48 registers spills: +0.7%). The 64-bit
-    // kernels: 8. They hold one class per lane in registers (a second slot
-    // lives in the level's stack copy, HiSlot): the undirected one then fits
-    // 64 registers with an 8-byte spill (C4 3.97 -> 3.62 s against 7 CTAs at
-    // 72 registers), the directed one spills less than with two slots (C3 -3%)
-    static constexpr int kMinBlocks = sizeof(W) == 4 ? 9 : 8;
+    // kernels hold one class per lane in registers (a second slot lives in
+    // the level's stack copy, HiSlot): the undirected one then fits 64
+    // registers at 8 CTAs/SM with an 8-byte spill (C4 3.97 -> 3.62 s against
+    // 7 CTAs at 72 registers); the directed one runs 7 (72 registers, 16 B
+    // stack, more shared memory per warp for its compacted subtrees: C3
+    // -0.9% time, +2% nodes/s against 8 at 64 registers with 48 B of spills)
+    static constexpr int kMinBlocks = sizeof(W) == 4 ? 9 : (DIR ? 7 : 8);
     // 64-bit kernel: a level whose live vertex sets fit 32 bits runs its
     // subtree compacted (CompactSearch, nested in the task) — 97% of C4's nodes
     static constexpr bool kNest = sizeof(W) == 8;
