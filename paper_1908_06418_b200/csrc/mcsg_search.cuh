@@ -292,8 +292,10 @@ struct CompactArea {
 
 // 64-bit kernel: a level of more than 32 classes keeps classes 32..63 (its
 // second slot) in its stack copy, not in registers; the policy reads them
-// through this (rare: none of C3's or C4's levels have more than 32 classes
-// outside labelled roots), so the hot loop holds one class per lane.
+// through this (rare: classes are disjoint and non-empty on both sides, so
+// more than 32 of them need more than 32 live vertices in G and in H — on
+// C3/C4 (n = 40/45) only levels near the top), so the hot loop holds one
+// class per lane.
 template <typename W>
 struct HiSlot {
     Cls<W>* lvl;  // the current level's classes (shared memory or the HBM spill area)
