@@ -151,7 +151,7 @@ struct Counters {
     unsigned long long ring_stall;   // a producer waited > 2 s for a ring slot (must stay 0)
     unsigned long long bad_task;     // a consumed subtree had an impossible header (must stay 0)
     unsigned long long frozen;       // subtrees frozen into the ring by restarts
-    unsigned long long nests_smem, nests_hbm;  // compacted subtrees (64-bit kernel)
+    unsigned long long nests_smem, nests_hbm;  // compacted subtrees (64-bit kernel; nests_hbm stays 0: shared-memory nests only)
     unsigned long long stall_pos, stall_head, stall_tail, stall_seq;  // its ticket and the ring state
     unsigned long long idle_cycles;  // Σ over warps of SM cycles spent waiting for a task
     unsigned long long busy_cycles;  // Σ over warps of SM cycles spent running tasks

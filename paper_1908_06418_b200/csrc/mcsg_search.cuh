@@ -287,7 +287,7 @@ struct CompactArea {
     // mv[0..1] = G low / high half, mv[2..3] = H low / high half
     alignas(16) uint32_t mv[4][8];
     uint64_t lg, lh;                 // the live sets
-    unsigned long long nests_smem, nests_hbm;  // subtrees run compacted, by stack placement
+    unsigned long long nests_smem, nests_hbm;  // subtrees run compacted, by stack placement (nests_hbm: 0 since nests are shared-memory only)
 };
 
 // 64-bit kernel: a level of more than 32 classes keeps classes 32..63 (its
